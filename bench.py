@@ -1,0 +1,437 @@
+"""bench.py -- GE-SpMM hot path on B200 (BASELINE.json metric:
+"SpMM GFLOP/s (2*nnz*N) and achieved HBM GB/s vs roofline at 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload config2|config1|config3-N|config4] [--op sum|max|min|mean]
+
+Workload (default, BASELINE configs[1]): R-MAT scale 20 (1M rows), 16M edges
+requested (Graph500 a/b/c = .57/.19/.19, deduplicated), x dense B with N=64,
+fp32, sum-reduce.  Synthetic data, seeded; generated on the GPU.
+
+A step = one execution of the hot path over the matrix with a cached plan
+(one kernel launch).  Each timed step is bracketed by CUDA events on the
+launching stream, with a 2x-L2 buffer written between steps (L2 flushed; the
+flush is outside the events).  N>1 (torchrun): row-block sharding, each rank
+runs its nnz-balanced row block after a one-time NCCL broadcast of B; time =
+max over ranks; value = total flops / that time ("strong" scaling).
+
+Extra keys: roofline (HBM, algorithmic compulsory bytes U per launch, see
+DESIGN.md), cpu_baseline (the oracle port on all host cores), e2e (host
+buffers through gespmm_csr_spmm_host: H2D + validate + plan + kernel + D2H),
+clocks (nvidia-smi sampled during the run), gpu_launches.
+
+--impl reference: the reference's own CPU implementation of the path (the
+unmodified raceset interpreter running gespmm_alg2.mir, oracle/_ref) on a
+bounded row sample of the same workload, all host threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--op", default="sum", choices=["sum", "max", "min", "mean"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--soak-s", type=float, default=1.5)
+    ap.add_argument("--ref-sample-products", type=int, default=800_000,
+                    help="--impl reference: nnz*N products per step (bounds interpreter RAM)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload_spec(name):
+    if name == "config2":
+        return dict(kind="rmat", scale=20, edges=16 * 2**20, N=64, seed=3,
+                    desc="R-MAT scale 20 (1M rows), 16M edges requested (dedup), N=64 (BASELINE configs[1])")
+    if name == "config4":
+        return dict(kind="rmat", scale=22, edges=64 * 2**20, N=128, seed=3,
+                    desc="R-MAT scale 22 (4M rows), 64M edges requested (dedup), N=128 (configs[3])")
+    if name == "config1":
+        return dict(kind="uniform", M=4096, K=4096, density=0.01, N=32, seed=1,
+                    desc="uniform 4096x4096, 1% density, N=32 (configs[0])")
+    if name.startswith("config3"):
+        N = int(name.split("-")[1]) if "-" in name else 64
+        return dict(kind="reddit", N=N, seed=5,
+                    desc=f"Reddit-like 232,965 rows ~114.6M nnz power-law, N={N} (configs[2])")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def make_workload(spec, device):
+    import numpy as np
+    import torch
+
+    from paper_2503_08946_b200 import workloads as W
+
+    if spec["kind"] == "rmat":
+        csr = W.rmat_csr(spec["scale"], spec["edges"], seed=spec["seed"], device=device)
+    elif spec["kind"] == "uniform":
+        c = W.uniform_csr(spec["M"], spec["K"], spec["density"], seed=spec["seed"])
+        csr = W.Csr(torch.as_tensor(c.rowptr, device=device), torch.as_tensor(c.colind, device=device),
+                    torch.as_tensor(c.vals, device=device), c.M, c.K)
+    else:
+        csr = W.reddit_like_csr(seed=spec["seed"], device=device)
+    B = W.dense_torch(csr.K, spec["N"], seed=2, device=device)
+    del np
+    return csr, B
+
+
+def algorithmic_bytes(M, K, N, nnz):
+    """compulsory bytes U and no-reuse gather bytes G."""
+    U = 4 * (M + 1) + 8 * nnz + 4 * K * N + 4 * M * N
+    G = 4 * (M + 1) + 8 * nnz + 4 * nnz * N + 4 * M * N
+    return U, G
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int, enabled: bool = True):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        if enabled:
+            try:
+                os.makedirs(os.path.dirname(self.path), exist_ok=True)
+                self.f = open(self.path, "w")
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={index}", f"--query-gpu={self.FIELDS}", "--format=csv",
+                     "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            except Exception:
+                self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9 or not parts[1].split()[0].isdigit():
+                    continue
+                sm.append(float(parts[1].split()[0]))
+                mx = max(mx, float(parts[2].split()[0]))
+                for nm, v in zip(names[1:], parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "window": "soak + timed region"}
+
+
+def cpu_baseline_port(csr, B, N, budget_s=2.5):
+    """The oracle's fp32 restatement (oracle/gespmm_oracle.c, OpenMP, all host
+    threads) on the full matrix, repeated for ~budget_s; best run."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    rp = csr.rowptr.cpu().numpy()
+    ci = csr.colind.cpu().numpy()
+    vv = csr.vals.cpu().numpy()
+    Bh = np.ascontiguousarray(B.cpu().numpy())
+    nth = O.num_threads()
+    best = None
+    t_end = time.perf_counter() + budget_s
+    runs = 0
+    while True:
+        t0 = time.perf_counter()
+        O.spmm_f32(rp, ci, vv, Bh, "sum", seg_len=256, nthreads=nth)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+        runs += 1
+        if time.perf_counter() > t_end or runs >= 20:
+            break
+    gflops = 2.0 * csr.nnz * N / best / 1e9
+    return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": nth, "kind": "port",
+            "sample": f"full workload (M={csr.M}, nnz={csr.nnz}, N={N}), best of {runs} runs, "
+                      f"oracle/gespmm_oracle.c fp32 twin, OpenMP {nth} threads"}
+
+
+def run_reference(args):
+    """Reference arm: the unmodified reference interpreter (oracle/_ref)."""
+    import numpy as np
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    spec = workload_spec(args.workload)
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libgespmm_ref.so not built (reference tree absent at build time)"}))
+        return 0
+    dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
+    csr, B = make_workload(spec, dev)
+    N = spec["N"]
+    rp = csr.rowptr.cpu().numpy().astype(np.int64)
+    ci = csr.colind.cpu().numpy()
+    vv = csr.vals.cpu().numpy()
+    Bh = np.ascontiguousarray(B.cpu().numpy())
+    nth = os.cpu_count() or 1
+    target_nnz = max(1, args.ref_sample_products // N)
+    M = csr.M
+    # step s samples the contiguous row block starting at a fixed stride offset
+    starts = np.linspace(0, M - 1, num=max(args.steps + args.warmup, 1), endpoint=False).astype(np.int64)
+
+    def sample(r0):
+        p0 = rp[r0]
+        r1 = int(np.searchsorted(rp, p0 + target_nnz, side="left"))
+        r1 = max(min(r1, M), r0 + 1)
+        return r0, r1
+
+    def step(i):
+        r0, r1 = sample(int(starts[i % len(starts)]))
+        p0, p1 = rp[r0], rp[r1]
+        srp = (rp[r0:r1 + 1] - p0).astype(np.int32)
+        _, secs, nlog = O.ref_spmm_csr(srp, ci[p0:p1], vv[p0:p1], Bh, nthreads=nth, want_c=False)
+        return int(p1 - p0), secs, nlog, r1 - r0
+
+    for i in range(args.warmup):
+        step(i)
+    tot_nnz, tot_s, tot_rows = 0, 0.0, 0
+    for i in range(args.steps):
+        n, s, _, rows = step(args.warmup + i)
+        tot_nnz += n
+        tot_s += s
+        tot_rows += rows
+    value = 2.0 * tot_nnz * N / tot_s / 1e9
+    line = {
+        "metric": "SpMM GFLOP/s (2*nnz*N)", "value": value, "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_s / max(args.steps, 1) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": spec["desc"], "op": "sum", "N": N, "M": M, "nnz": csr.nnz},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": nth, "kind": "reference",
+                         "sample": f"per step a contiguous row block with ~{target_nnz} nnz "
+                                   f"(avg {tot_rows / max(args.steps, 1):.0f} rows) of the same "
+                                   f"matrix; raceset::run on gespmm_alg2.mir (block 4, grid "
+                                   f"rows x N/4), rows split into {nth} parallel instances; "
+                                   f"time = run() calls only"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_08946_b200.spmm import Plan, csr_spmm_host, partition_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    spec = workload_spec(args.workload)
+    N = spec["N"]
+    csr, B = make_workload(spec, dev)
+    M_all, K, nnz_all = csr.M, csr.K, csr.nnz
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- row-block sharding (world > 1) ----------------------------------
+    if world > 1:
+        rp_h = csr.rowptr.cpu().numpy()
+        bounds = partition_rows(rp_h, world)
+        a, b = int(bounds[rank]), int(bounds[rank + 1])
+        p0, p1 = int(rp_h[a]), int(rp_h[b])
+        rowptr = (csr.rowptr[a:b + 1] - p0).contiguous()
+        colind = csr.colind[p0:p1].contiguous()
+        vals = csr.vals[p0:p1].contiguous()
+        if rank != 0:
+            B.zero_()  # only the root holds B; the broadcast is the exchange step
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dist.broadcast(B, src=0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bcast_ms = e0.elapsed_time(e1)
+    else:
+        rowptr, colind, vals = csr.rowptr, csr.colind, csr.vals
+        bcast_ms = 0.0
+    M_loc, nnz_loc = rowptr.numel() - 1, colind.numel()
+
+    # ---- plan (cached across steps; its build is reported separately) ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    plan = Plan(rowptr, colind, K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    plan_ms = e0.elapsed_time(e1)
+    plan_wall_ms = (time.perf_counter() - t0) * 1e3
+    info = plan.info()
+    C = torch.empty((M_loc, N), dtype=torch.float32, device=dev)
+
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+
+    def run_once():
+        plan.execute(vals, B, args.op, out=C, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        run_once()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local, enabled=not args.no_clocks and rank == 0)
+    # soak: back-to-back launches so the clock samples see the kernel under load
+    t_soak = time.perf_counter() + (args.soak_s if clocks.proc is not None else 0.0)
+    while time.perf_counter() < t_soak:
+        for _ in range(50):
+            run_once()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        starts[i].record(stream)
+        run_once()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    clk = clocks.stop()
+    t_mean = sum(times) / len(times)
+    t_max = torch.tensor([t_mean], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_job = float(t_max.item())  # ms, max over ranks
+
+    flops = 2.0 * nnz_all * N
+    value = flops / (t_job * 1e-3) / 1e9
+    U, G = algorithmic_bytes(M_loc, K, N, nnz_loc)
+    peak, peak_src = peaks()
+    achieved = U / (t_mean * 1e-3) / 1e9
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"{args.workload}:{args.op}")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public host API (H2D + validate + plan + kernel + D2H)
+    e2e = None
+    if not args.no_e2e:
+        hp = lambda t: t.cpu().pin_memory()  # noqa: E731
+        h_rp, h_ci, h_v, h_B = hp(rowptr), hp(colind), hp(vals), hp(B)
+        h_C = torch.empty((M_loc, N), dtype=torch.float32).pin_memory()
+        csr_spmm_host(h_rp, h_ci, h_v, h_B, args.op, out=h_C)  # warm
+        reps = max(3, min(args.steps, 10))
+        et = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            csr_spmm_host(h_rp, h_ci, h_v, h_B, args.op, out=h_C)
+            et.append(time.perf_counter() - t0)
+        e2e_t = torch.tensor([sum(et) / len(et)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops / float(e2e_t.item()) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(4 * (M_loc + 1) + 8 * nnz_loc + 4 * K * N),
+               "d2h_bytes_per_step": int(4 * M_loc * N),
+               "ms_per_step": float(e2e_t.item()) * 1e3,
+               "path": "gespmm_csr_spmm_host (pinned host buffers; H2D, device CSR validation, "
+                       "plan, kernel, D2H; wall clock per call)"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(csr, B, N)
+
+    if rank == 0:
+        line = {
+            "metric": "SpMM GFLOP/s (2*nnz*N)",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_job, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": spec["desc"], "op": args.op, "N": N, "M": M_all, "K": K,
+                       "nnz": nnz_all, "l2_flush": f"{flush.numel() * 4 >> 20} MiB written between timed steps",
+                       "parallelism": f"row-block x{world}" if world > 1 else "single GPU",
+                       "plan": {"n_items": info["n_items"], "n_long_rows": info["n_long_rows"],
+                                "n_segments": info["n_segments"], "build_ms": plan_ms,
+                                "build_wall_ms": plan_wall_ms},
+                       "b_broadcast_ms": bcast_ms},
+            "hbm_gbs_algorithmic": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_model": f"U = 4(M+1) + 8nnz + 4KN + 4MN = {U} B per launch",
+                         "peak_source": peak_src,
+                         "gather_bytes_G": G, "gather_GBs": G / (t_mean * 1e-3) / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]),
+            "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,198 @@
+/*
+ * gespmm.h -- C-ABI of the B200-native GE-SpMM hot path (libgespmm.so).
+ *
+ * Drop-in boundary for the reference's CSR x dense SpMM path.  The reference
+ * (arXiv 2503.08946's `raceset` artifact) exposes that path as
+ *
+ *   kernel @gespmm_alg2(%rowPtr: i32*, %colInd: i32*, %val: f32*, %B: f32*,
+ *                       %C: f32*, %M, %N, %K)
+ *        -- /root/reference/proj/fixtures/gespmm_alg2.mir:5
+ *   raceset::run(const ConcreteInstance&, const Function&, const RunOptions&)
+ *        -- /root/reference/proj/include/raceset/oracle.hpp:71-74
+ *   raceset::validate_instance(const ConcreteInstance&)   (CSR contract)
+ *        -- /root/reference/proj/include/raceset/oracle.hpp:38-39,
+ *           src/oracle.cpp:291-316
+ *
+ * Conventions:
+ *   - CSR: rowptr int32[M+1], colind int32[nnz], vals fp32[nnz]; colind need
+ *     not be sorted or unique (the reference does not require it).
+ *   - B fp32 [K x N] row-major with leading dimension ldb >= N; C fp32 [M x N]
+ *     row-major with ldc >= N (gespmm_alg2.mir:51-56 uses ld = N).
+ *   - 64-bit sizes and 64-bit B/C address arithmetic (K*N may exceed 2^31).
+ *   - Device pointers are caller-owned; nothing is copied behind the caller's
+ *     back; work is enqueued on `stream` (a cudaStream_t, 0 = legacy default).
+ *   - No exceptions cross the ABI: every entry point returns a status; the
+ *     thread-local detail string is gespmm_last_error().
+ *   - Thread safety: distinct plans may be used concurrently from distinct
+ *     threads; one plan must not be executed concurrently with itself.
+ *
+ * Semantics (normative, oracle/gespmm_oracle.c):
+ *   per output cell (i, j), nonzeros are reduced in ascending p, fp32.
+ *   SUM : acc = fmaf(val[p], B[col[p]][j], acc) from acc = 0 (accumulate: C0)
+ *   MEAN: SUM from 0, then acc / deg(i) (correctly rounded); accumulate adds C0
+ *   MAX/MIN: m = val[p]*B[col[p]][j] (rounded, unfused); acc = first m, then
+ *         acc = (m > acc) ? m : acc   (MIN: <); accumulate seeds acc = C0
+ *   empty rows give 0 (accumulate: C0 for sum/max/min, C0 + 0 for mean).
+ *   Rows with more than GESPMM_SEGMENT_LEN nonzeros are reduced in fixed
+ *   GESPMM_SEGMENT_LEN-long segments from the row start, combined strictly left
+ *   to right (sum/mean: +, max/min: the same comparison).  Results are
+ *   deterministic and independent of device, grid and sharding.
+ */
+#ifndef GESPMM_H_
+#define GESPMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GESPMM_VERSION_MAJOR 0
+#define GESPMM_VERSION_MINOR 1
+/* Long-row segment length (nonzeros).  Part of the numerical contract. */
+#define GESPMM_SEGMENT_LEN 256
+
+/* Status codes.  Mirrors the reference's ErrorKind values that can arise on
+ * this path (reference include/raceset/error.hpp:10-32):
+ *   CsrInvalid -> GESPMM_CSR_INVALID (src/oracle.cpp:291-316),
+ *   OutOfBounds -> GESPMM_OUT_OF_BOUNDS (src/oracle.cpp:673-677),
+ * plus the host-API failures a C-ABI needs. */
+typedef enum gespmm_status {
+  GESPMM_OK = 0,
+  GESPMM_CSR_INVALID = 1,
+  GESPMM_OUT_OF_BOUNDS = 2,
+  GESPMM_INVALID_ARG = 3,
+  GESPMM_CUDA_ERROR = 4,
+  GESPMM_NCCL_ERROR = 5,
+  GESPMM_NOT_SUPPORTED = 6
+} gespmm_status_t;
+
+/* Reduce operator (compile-time functor inside the kernels).  The reference
+ * has SUM only (gespmm_alg2.mir:57-59); MAX/MIN/MEAN are the generalized
+ * semiring of BASELINE.json's north star. */
+typedef enum gespmm_reduce {
+  GESPMM_REDUCE_SUM = 0,
+  GESPMM_REDUCE_MAX = 1,
+  GESPMM_REDUCE_MIN = 2,
+  GESPMM_REDUCE_MEAN = 3
+} gespmm_reduce_t;
+
+typedef struct gespmm_plan_s* gespmm_plan_t;
+
+/* Library version as MAJOR*100 + MINOR. */
+int gespmm_version(void);
+/* Static description of a status code. */
+const char* gespmm_status_string(gespmm_status_t s);
+/* Detail of the last failure on the calling thread ("" if none), in the style
+ * of raceset::Error::what() ("invalid csr: rowPtr must be nondecreasing"). */
+const char* gespmm_last_error(void);
+
+/* Host-side CSR validation with the reference's rules
+ * (validate_instance, src/oracle.cpp:291-316): rowptr non-empty, rowptr[0] == 0,
+ * nondecreasing, rowptr[rowptr_len-1] == colind_len, colind_len == vals_len,
+ * 0 <= colind < K.  Added: rowptr_len == M + 1.  Pointers are HOST memory. */
+gespmm_status_t gespmm_validate_csr(int64_t M, int64_t K, int64_t rowptr_len,
+                                    const int32_t* rowptr, int64_t colind_len,
+                                    const int32_t* colind, int64_t vals_len);
+
+/* The same rules checked on the GPU for DEVICE pointers (one pass over rowptr
+ * and colind; synchronizes `stream` to return the verdict). */
+gespmm_status_t gespmm_validate_csr_device(int64_t M, int64_t K, int64_t nnz,
+                                           const int32_t* rowptr, const int32_t* colind,
+                                           void* stream);
+
+/* One-shot SpMM on device buffers: C = A (op) B, or C = C0 (op-combine) A (op) B
+ * when accumulate != 0 (the reference kernel's C read-modify-write,
+ * gespmm_alg2.mir:55-59).  Validates the CSR on the device (the reference
+ * validates inside run(), src/oracle.cpp:700), builds a temporary plan,
+ * launches, and releases the plan stream-ordered.  Synchronizes once (plan). */
+gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
+                                const int32_t* rowptr, const int32_t* colind,
+                                const float* vals, const float* B, int64_t ldb, float* C,
+                                int64_t ldc, gespmm_reduce_t op, int accumulate, void* stream);
+
+/* One-shot SpMM on HOST buffers (the C++-host drop-in for raceset::run, which
+ * takes its instance by value, src/oracle.cpp:381-399): copies the CSR and B
+ * to the device, validates, plans, computes and copies C back (C is read first
+ * when accumulate != 0).  Blocking; `stream` may be 0.  Host buffers may be
+ * pageable; pinned buffers copy at full link speed. */
+gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
+                                     const int32_t* rowptr, const int32_t* colind,
+                                     const float* vals, const float* B, int64_t ldb, float* C,
+                                     int64_t ldc, gespmm_reduce_t op, int accumulate,
+                                     void* stream);
+
+/* Plan = the nnz-balanced work decomposition of one sparsity structure
+ * (tiles of consecutive short rows + fixed segments of long rows), built on
+ * the GPU.  Depends only on (M, nnz, rowptr); reusable for any vals/B/N/op.
+ * flags: bit 0 = also validate colind against K on the device.
+ * Synchronizes `stream` once to size the work list. */
+gespmm_status_t gespmm_plan_create(gespmm_plan_t* plan, int64_t M, int64_t K, int64_t nnz,
+                                   const int32_t* rowptr, const int32_t* colind, int flags,
+                                   void* stream);
+/* Launch with a plan (asynchronous on `stream`, no host synchronization). */
+gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t* rowptr,
+                                    const int32_t* colind, const float* vals, const float* B,
+                                    int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                    int accumulate, void* stream);
+gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan);
+
+/* Plan introspection (tests, benches). */
+typedef struct gespmm_plan_info {
+  int64_t M, nnz;
+  int64_t n_items;        /* work items (short-row tiles + long-row segments) */
+  int64_t n_tiles;        /* short-row tiles */
+  int64_t n_long_rows;    /* rows with deg > GESPMM_SEGMENT_LEN */
+  int64_t n_segments;     /* segments of long rows */
+  int64_t segment_len;    /* GESPMM_SEGMENT_LEN */
+  int64_t tile_work;      /* target work units per tile */
+  int64_t kernel_launches_per_execute;
+} gespmm_plan_info_t;
+gespmm_status_t gespmm_plan_get_info(gespmm_plan_t plan, gespmm_plan_info_t* info);
+
+/* Which kernel variant a given N / alignment selects ("vec4_lpr32_cwm2", ...),
+ * and a test-only override ("" = heuristic).  Not thread-safe. */
+const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const float* C,
+                                int64_t ldc);
+gespmm_status_t gespmm_set_variant_override(const char* name);
+
+/* nnz-balanced row partition for row-block sharding over `parts` ranks
+ * (HOST rowptr): bounds[0..parts] with bounds[0] = 0, bounds[parts] = M,
+ * cut so that (nnz + rows) per part is balanced.  Rows never span parts. */
+gespmm_status_t gespmm_partition_rows(int64_t M, const int32_t* rowptr, int parts,
+                                      int64_t* bounds);
+
+/* ---- multi-GPU (row-block sharding) -------------
+ * NCCL is resolved at run time (dlopen "libnccl.so.2"; the copy already loaded
+ * in the process wins), so the library never drags in a second NCCL. */
+
+/* NCCL unique id (128 bytes) for gespmm_comm_init; call on one rank and ship
+ * the bytes to the others out of band. */
+gespmm_status_t gespmm_comm_get_unique_id(char id[128]);
+/* Creates an ncclComm_t on the current device; *comm receives it. */
+gespmm_status_t gespmm_comm_init(void** comm, int world, const char id[128], int rank);
+gespmm_status_t gespmm_comm_destroy(void* comm);
+
+/* Row-sharded SpMM on `comm`.  Each rank passes its row block of the CSR
+ * (rowptr rebased to 0, M_local rows) and a B buffer of K x N (ldb); B is
+ * broadcast from `root` over NVLink (ncclBroadcast, in place) -- the only
+ * exchange -- then each rank computes its C slab (M_local x N, ldc).  If
+ * C_full != NULL, the slabs are additionally all-gathered into C_full
+ * (M_global x N, ld = ldc_full) with one ncclBroadcast per slab owner, using
+ * row_bounds[0..world] (global row offsets of every rank's slab).  `plan`
+ * may be NULL (a temporary plan is built).  Asynchronous on `stream` except
+ * for temporary-plan creation. */
+gespmm_status_t gespmm_sharded_spmm(void* comm, int world, int rank, int root,
+                                    gespmm_plan_t plan, int64_t M_local, int64_t K, int64_t N,
+                                    int64_t nnz_local, const int32_t* rowptr,
+                                    const int32_t* colind, const float* vals, float* B,
+                                    int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                    int accumulate, float* C_full, int64_t ldc_full,
+                                    const int64_t* row_bounds, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GESPMM_H_ */

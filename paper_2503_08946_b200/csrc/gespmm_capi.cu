@@ -1,0 +1,372 @@
+// gespmm_capi.cu -- the extern "C" boundary (include/gespmm.h).
+//
+// Replaces the reference's hot-path surface:
+//   raceset::validate_instance  (src/oracle.cpp:291-316)  -> gespmm_validate_csr[_device]
+//   raceset::run on gespmm_alg2 (src/oracle.cpp:699-736)  -> gespmm_csr_spmm[_host]
+// Reference errors are C++ exceptions raceset::Error{ErrorKind}
+// (include/raceset/error.hpp:36-56); here they are status codes plus a
+// thread-local detail string with the same wording.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "gespmm_internal.h"
+
+namespace gespmm {
+
+gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* colind,
+                           bool check_colind, cudaStream_t s);
+gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K, cudaStream_t s);
+
+namespace {
+thread_local std::string g_last_error;
+std::string g_variant_override;  // test hook; "" = heuristic
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+gespmm_status_t fail(gespmm_status_t s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+gespmm_status_t cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return GESPMM_CUDA_ERROR;
+}
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Shape/argument checks shared by the device and host entry points.
+gespmm_status_t check_shape(int64_t M, int64_t K, int64_t N, int64_t nnz, int64_t ldb,
+                            int64_t ldc) {
+  if (M < 0 || K < 0 || N < 1 || nnz < 0)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: need M, K, nnz >= 0 and N >= 1");
+  if (ldb < N || ldc < N) return fail(GESPMM_INVALID_ARG, "invalid argument: ldb and ldc must be >= N");
+  // int32 indices: nonzero positions and rows are int32 (gespmm_alg2.mir:5 i32
+  // params); leave headroom for the 128-wide staging arithmetic.
+  if (nnz > (int64_t(1) << 31) - 1024 || M > (int64_t(1) << 31) - 2 || K > (int64_t(1) << 31) - 1)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: M, K and nnz must fit int32 indexing");
+  return GESPMM_OK;
+}
+
+Variant pick_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc) {
+  Variant v = choose_variant(N, B, ldb, C, ldc);
+  if (!g_variant_override.empty()) {
+    Variant o;
+    if (parse_variant(g_variant_override.c_str(), &o)) {
+      auto ok = [&](int vec) {
+        const uintptr_t a = static_cast<uintptr_t>(vec) * 4;
+        return reinterpret_cast<uintptr_t>(B) % a == 0 && reinterpret_cast<uintptr_t>(C) % a == 0 &&
+               ldb % vec == 0 && ldc % vec == 0 && N % vec == 0;
+      };
+      if (ok(o.vec)) v = o;
+    }
+  }
+  return v;
+}
+
+gespmm_status_t ensure_workspace(gespmm_plan_s* plan, int64_t ldp, int ncb, cudaStream_t s) {
+  if (plan->n_segs == 0) return GESPMM_OK;
+  const int64_t need_p = plan->n_segs * ldp;
+  if (need_p > plan->partial_floats) {
+    if (plan->partials) cudaFree(plan->partials);
+    plan->partials = nullptr;
+    plan->partial_floats = 0;
+    cudaError_t e = cudaMalloc(&plan->partials, static_cast<size_t>(need_p) * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "plan partials");
+    plan->partial_floats = need_p;
+  }
+  const int64_t need_c = plan->n_segs * ncb;
+  if (need_c > plan->counter_ints) {
+    if (plan->counters) cudaFree(plan->counters);
+    plan->counters = nullptr;
+    plan->counter_ints = 0;
+    cudaError_t e = cudaMalloc(&plan->counters, static_cast<size_t>(need_c) * sizeof(int));
+    if (e != cudaSuccess) return cuda_fail(e, "plan counters");
+    e = cudaMemsetAsync(plan->counters, 0, static_cast<size_t>(need_c) * sizeof(int), s);
+    if (e != cudaSuccess) return cuda_fail(e, "plan counters memset");
+    plan->counter_ints = need_c;
+  }
+  return GESPMM_OK;
+}
+
+}  // namespace
+}  // namespace gespmm
+
+using namespace gespmm;
+
+extern "C" {
+
+int gespmm_version(void) { return GESPMM_VERSION_MAJOR * 100 + GESPMM_VERSION_MINOR; }
+
+const char* gespmm_status_string(gespmm_status_t s) {
+  switch (s) {
+    case GESPMM_OK: return "ok";
+    case GESPMM_CSR_INVALID: return "invalid csr";          // ErrorKind::CsrInvalid
+    case GESPMM_OUT_OF_BOUNDS: return "out of bounds";      // ErrorKind::OutOfBounds
+    case GESPMM_INVALID_ARG: return "invalid argument";
+    case GESPMM_CUDA_ERROR: return "cuda error";
+    case GESPMM_NCCL_ERROR: return "nccl error";
+    case GESPMM_NOT_SUPPORTED: return "not supported";
+  }
+  return "unknown status";
+}
+
+const char* gespmm_last_error(void) { return g_last_error.c_str(); }
+
+gespmm_status_t gespmm_validate_csr(int64_t M, int64_t K, int64_t rowptr_len,
+                                    const int32_t* rowptr, int64_t colind_len,
+                                    const int32_t* colind, int64_t vals_len) {
+  g_last_error.clear();
+  if (M < 0 || K < 0 || rowptr_len < 0 || colind_len < 0 || vals_len < 0)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: negative size");
+  if ((rowptr_len > 0 && !rowptr) || (colind_len > 0 && !colind))
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
+  // reference src/oracle.cpp:302-315, in the same order
+  if (rowptr_len == 0 || rowptr[0] != 0) return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr[0] must be 0");
+  for (int64_t i = 1; i < rowptr_len; ++i)
+    if (rowptr[i] < rowptr[i - 1])
+      return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr must be nondecreasing");
+  if (static_cast<int64_t>(rowptr[rowptr_len - 1]) != colind_len)
+    return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr end differs from nnz of colInd");
+  if (colind_len != vals_len)
+    return fail(GESPMM_CSR_INVALID, "invalid csr: colInd and val lengths differ");
+  for (int64_t p = 0; p < colind_len; ++p)
+    if (colind[p] < 0 || colind[p] >= K)
+      return fail(GESPMM_CSR_INVALID,
+                  "invalid csr: colInd entry out of [0," + std::to_string(K) + ")");
+  // added: the kernel reads rowPtr[i+1] for every row i < M (gespmm_alg2.mir:16-18)
+  if (rowptr_len != M + 1) return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr length must be M + 1");
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_validate_csr_device(int64_t M, int64_t K, int64_t nnz,
+                                           const int32_t* rowptr, const int32_t* colind,
+                                           void* stream) {
+  g_last_error.clear();
+  if (M < 0 || K < 0 || nnz < 0) return fail(GESPMM_INVALID_ARG, "invalid argument: negative size");
+  gespmm_plan_s tmp;
+  tmp.M = M;
+  tmp.K = K;
+  tmp.nnz = nnz;
+  gespmm_status_t st = build_plan(&tmp, rowptr, colind, true, as_stream(stream));
+  if (tmp.items) cudaFree(tmp.items);
+  return st;
+}
+
+gespmm_status_t gespmm_plan_create(gespmm_plan_t* plan, int64_t M, int64_t K, int64_t nnz,
+                                   const int32_t* rowptr, const int32_t* colind, int flags,
+                                   void* stream) {
+  g_last_error.clear();
+  if (!plan) return fail(GESPMM_INVALID_ARG, "invalid argument: plan is null");
+  *plan = nullptr;
+  gespmm_status_t st = check_shape(M, K, 1, nnz, 1, 1);
+  if (st != GESPMM_OK) return st;
+  if (M > 0 && !rowptr) return fail(GESPMM_INVALID_ARG, "invalid argument: rowptr is null");
+  auto* p = new gespmm_plan_s();
+  p->M = M;
+  p->K = K;
+  p->nnz = nnz;
+  cudaGetDevice(&p->device);
+  st = build_plan(p, rowptr, colind, (flags & 1) != 0, as_stream(stream));
+  if (st != GESPMM_OK) {
+    gespmm_plan_destroy(p);
+    return st;
+  }
+  *plan = p;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t* rowptr,
+                                    const int32_t* colind, const float* vals, const float* B,
+                                    int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                    int accumulate, void* stream) {
+  if (!plan) return fail(GESPMM_INVALID_ARG, "invalid argument: plan is null");
+  gespmm_status_t st = check_shape(plan->M, plan->K, N, plan->nnz, ldb, ldc);
+  if (st != GESPMM_OK) return st;
+  if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
+  if (plan->n_items == 0) return GESPMM_OK;  // M == 0
+  cudaStream_t s = as_stream(stream);
+  const Variant v = pick_variant(N, B, ldb, C, ldc);
+  const int ncb = static_cast<int>((N + variant_cols(v) - 1) / variant_cols(v));
+  if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
+  const int64_t ldp = (N + 3) & ~int64_t(3);
+  st = ensure_workspace(plan, ldp, ncb, s);
+  if (st != GESPMM_OK) return st;
+  KParams p{};
+  p.rowptr = rowptr;
+  p.colind = colind;
+  p.vals = vals;
+  p.B = B;
+  p.C = C;
+  p.ldb = ldb;
+  p.ldc = ldc;
+  p.N = N;
+  p.ldp = ldp;
+  p.items = plan->items;
+  p.n_items = plan->n_items;
+  p.M = static_cast<int>(plan->M);
+  p.nnz = static_cast<int>(plan->nnz);
+  p.partials = plan->partials;
+  p.counters = plan->counters;
+  p.accumulate = accumulate ? 1 : 0;
+  p.ncb = ncb;
+  p.idx_aligned = (reinterpret_cast<uintptr_t>(colind) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(vals) % 16 == 0);
+  cudaError_t e = launch_spmm(op, v, p, s);
+  if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
+  if (!plan) return GESPMM_OK;
+  if (plan->items) cudaFree(plan->items);
+  if (plan->partials) cudaFree(plan->partials);
+  if (plan->counters) cudaFree(plan->counters);
+  delete plan;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_plan_get_info(gespmm_plan_t plan, gespmm_plan_info_t* info) {
+  if (!plan || !info) return fail(GESPMM_INVALID_ARG, "invalid argument: null");
+  info->M = plan->M;
+  info->nnz = plan->nnz;
+  info->n_items = plan->n_items;
+  info->n_tiles = plan->n_tiles;
+  info->n_long_rows = plan->n_long;
+  info->n_segments = plan->n_segs;
+  info->segment_len = kSeg;
+  info->tile_work = kTileWork;
+  info->kernel_launches_per_execute = plan->n_items > 0 ? 1 : 0;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
+                                const int32_t* rowptr, const int32_t* colind,
+                                const float* vals, const float* B, int64_t ldb, float* C,
+                                int64_t ldc, gespmm_reduce_t op, int accumulate, void* stream) {
+  g_last_error.clear();
+  gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
+  if (st != GESPMM_OK) return st;
+  gespmm_plan_t plan = nullptr;
+  st = gespmm_plan_create(&plan, M, K, nnz, rowptr, colind, /*validate colind*/ 1, stream);
+  if (st != GESPMM_OK) return st;
+  st = gespmm_plan_execute(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, stream);
+  // plan memory is released once the launch has drained
+  cudaStreamSynchronize(as_stream(stream));
+  gespmm_plan_destroy(plan);
+  return st;
+}
+
+gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
+                                     const int32_t* rowptr, const int32_t* colind,
+                                     const float* vals, const float* B, int64_t ldb, float* C,
+                                     int64_t ldc, gespmm_reduce_t op, int accumulate,
+                                     void* stream) {
+  g_last_error.clear();
+  gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
+  if (st != GESPMM_OK) return st;
+  cudaStream_t s = as_stream(stream);
+  // device copies: B and C packed with ld = N
+  int32_t* d_rp = nullptr;
+  int32_t* d_ci = nullptr;
+  float* d_v = nullptr;
+  float* d_B = nullptr;
+  float* d_C = nullptr;
+  auto cleanup = [&]() {
+    cudaFreeAsync(d_rp, s);
+    cudaFreeAsync(d_ci, s);
+    cudaFreeAsync(d_v, s);
+    cudaFreeAsync(d_B, s);
+    cudaFreeAsync(d_C, s);
+    cudaStreamSynchronize(s);
+  };
+  cudaError_t e = cudaSuccess;
+  auto al = [&](auto** p, size_t n) {
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(p), n > 0 ? n : 16, s);
+  };
+  al(&d_rp, static_cast<size_t>(M + 1) * 4);
+  al(&d_ci, static_cast<size_t>(nnz) * 4);
+  al(&d_v, static_cast<size_t>(nnz) * 4);
+  al(&d_B, static_cast<size_t>(K * N) * 4);
+  al(&d_C, static_cast<size_t>(M * N) * 4);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "device allocation");
+  }
+  auto h2d = [&](void* d, const void* h, size_t n) {
+    if (e == cudaSuccess && n) e = cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s);
+  };
+  h2d(d_rp, rowptr, static_cast<size_t>(M + 1) * 4);
+  h2d(d_ci, colind, static_cast<size_t>(nnz) * 4);
+  h2d(d_v, vals, static_cast<size_t>(nnz) * 4);
+  if (e == cudaSuccess && K * N > 0)
+    e = cudaMemcpy2DAsync(d_B, N * 4, B, ldb * 4, N * 4, K, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && accumulate && M * N > 0)
+    e = cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "host to device copy");
+  }
+  gespmm_plan_t plan = nullptr;
+  st = gespmm_plan_create(&plan, M, K, nnz, d_rp, d_ci, 1, stream);
+  if (st == GESPMM_OK)
+    st = gespmm_plan_execute(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate, stream);
+  if (st == GESPMM_OK && M * N > 0) {
+    e = cudaMemcpy2DAsync(C, ldc * 4, d_C, N * 4, N * 4, M, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_fail(e, "device to host copy");
+  }
+  if (plan) {
+    cudaStreamSynchronize(s);
+    gespmm_plan_destroy(plan);
+  }
+  cleanup();
+  return st;
+}
+
+const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const float* C,
+                                int64_t ldc) {
+  static thread_local std::string name;
+  name = variant_name(pick_variant(N, B, ldb, C, ldc));
+  return name.c_str();
+}
+
+gespmm_status_t gespmm_set_variant_override(const char* name) {
+  if (!name || !*name) {
+    g_variant_override.clear();
+    return GESPMM_OK;
+  }
+  Variant v;
+  if (!parse_variant(name, &v)) return fail(GESPMM_INVALID_ARG, std::string("unknown variant ") + name);
+  g_variant_override = name;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_partition_rows(int64_t M, const int32_t* rowptr, int parts,
+                                      int64_t* bounds) {
+  if (M < 0 || parts < 1 || !rowptr || !bounds)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: partition_rows");
+  // balance nnz + rows (a row's C store costs about one nonzero's gather)
+  const int64_t total = static_cast<int64_t>(rowptr[M]) + M;
+  bounds[0] = 0;
+  for (int r = 1; r < parts; ++r) {
+    const int64_t target = total * r / parts;
+    int64_t lo = bounds[r - 1], hi = M;
+    while (lo < hi) {  // first row i with rowptr[i] + i >= target
+      const int64_t mid = (lo + hi) / 2;
+      if (static_cast<int64_t>(rowptr[mid]) + mid < target) lo = mid + 1;
+      else hi = mid;
+    }
+    bounds[r] = lo;
+  }
+  bounds[parts] = M;
+  return GESPMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+// gespmm_comm.cu -- row-block sharding over NVLink/NVSwitch.
+//
+// The path's only exchange step is the broadcast of B: every C row depends
+// only on its own CSR row and B, so each rank computes its C slab from its row
+// block with no collective inside the compute.  B goes out once with
+// ncclBroadcast (NVLink 5 / NVSwitch; NVLS when NCCL enables it); the optional
+// C all-gather is one grouped ncclBroadcast per slab owner (slabs are uneven).
+// Per-row reduction order is untouched by sharding and the plan depends only on
+// rowptr, so results are bit-identical at 1/2/4/8 GPUs.
+//
+// NCCL is resolved at run time: if the process already loaded a libnccl.so.2
+// (e.g. torch's), dlopen returns that copy, so two NCCLs never coexist.
+#include <dlfcn.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "gespmm_internal.h"
+
+namespace {
+
+typedef int nccl_result_t;
+typedef struct {
+  char internal[128];
+} nccl_unique_id_t;
+typedef void* nccl_comm_t;
+
+struct Nccl {
+  nccl_result_t (*GetUniqueId)(nccl_unique_id_t*) = nullptr;
+  nccl_result_t (*CommInitRank)(nccl_comm_t*, int, nccl_unique_id_t, int) = nullptr;
+  nccl_result_t (*CommDestroy)(nccl_comm_t) = nullptr;
+  nccl_result_t (*Broadcast)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  nccl_result_t (*GroupStart)() = nullptr;
+  nccl_result_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(nccl_result_t) = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+constexpr int kNcclChar = 0;  // ncclChar / ncclInt8: byte-wise broadcast
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      n.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* name) { return dlsym(h, name); };
+    n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
+    n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
+    n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
+    n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(sym("ncclBroadcast"));
+    n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
+    n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(sym("ncclGroupEnd"));
+    n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Broadcast && n.GroupStart &&
+           n.GroupEnd && n.GetErrorString;
+    if (!n.ok) n.why = "libnccl.so.2 lacks required symbols";
+  });
+  return n;
+}
+
+gespmm_status_t nccl_fail(nccl_result_t r, const char* what) {
+  Nccl& n = nccl();
+  return gespmm::fail(GESPMM_NCCL_ERROR,
+                      std::string(what) + ": " + (n.GetErrorString ? n.GetErrorString(r) : "?"));
+}
+
+}  // namespace
+
+extern "C" {
+
+gespmm_status_t gespmm_comm_get_unique_id(char id[128]) {
+  Nccl& n = nccl();
+  if (!n.ok) return gespmm::fail(GESPMM_NOT_SUPPORTED, n.why);
+  nccl_unique_id_t u;
+  nccl_result_t r = n.GetUniqueId(&u);
+  if (r != 0) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id, u.internal, 128);
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_comm_init(void** comm, int world, const char id[128], int rank) {
+  Nccl& n = nccl();
+  if (!n.ok) return gespmm::fail(GESPMM_NOT_SUPPORTED, n.why);
+  if (!comm || world < 1 || rank < 0 || rank >= world)
+    return gespmm::fail(GESPMM_INVALID_ARG, "invalid argument: comm_init");
+  nccl_unique_id_t u;
+  std::memcpy(u.internal, id, 128);
+  nccl_comm_t c = nullptr;
+  nccl_result_t r = n.CommInitRank(&c, world, u, rank);
+  if (r != 0) return nccl_fail(r, "ncclCommInitRank");
+  *comm = c;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_comm_destroy(void* comm) {
+  Nccl& n = nccl();
+  if (!comm) return GESPMM_OK;
+  if (!n.ok) return gespmm::fail(GESPMM_NOT_SUPPORTED, n.why);
+  nccl_result_t r = n.CommDestroy(comm);
+  if (r != 0) return nccl_fail(r, "ncclCommDestroy");
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_sharded_spmm(void* comm, int world, int rank, int root,
+                                    gespmm_plan_t plan, int64_t M_local, int64_t K, int64_t N,
+                                    int64_t nnz_local, const int32_t* rowptr,
+                                    const int32_t* colind, const float* vals, float* B,
+                                    int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                    int accumulate, float* C_full, int64_t ldc_full,
+                                    const int64_t* row_bounds, void* stream) {
+  Nccl& n = nccl();
+  if (!n.ok) return gespmm::fail(GESPMM_NOT_SUPPORTED, n.why);
+  if (!comm || world < 1 || rank < 0 || rank >= world || root < 0 || root >= world)
+    return gespmm::fail(GESPMM_INVALID_ARG, "invalid argument: comm/world/rank/root");
+  if (ldb != N) return gespmm::fail(GESPMM_INVALID_ARG, "invalid argument: sharded B needs ldb == N");
+  if (C_full && (!row_bounds || ldc != N || ldc_full != N))
+    return gespmm::fail(GESPMM_INVALID_ARG,
+                        "invalid argument: C all-gather needs row_bounds and ldc == ldc_full == N");
+  if (C_full && row_bounds[rank + 1] - row_bounds[rank] != M_local)
+    return gespmm::fail(GESPMM_INVALID_ARG, "invalid argument: row_bounds disagree with M_local");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // 1. the exchange: B from root, in place
+  nccl_result_t r = n.Broadcast(B, B, static_cast<size_t>(K * N) * sizeof(float), kNcclChar, root,
+                                comm, s);
+  if (r != 0) return nccl_fail(r, "ncclBroadcast(B)");
+  // 2. the local slab
+  gespmm_plan_t p = plan;
+  gespmm_status_t st = GESPMM_OK;
+  if (!p) st = gespmm_plan_create(&p, M_local, K, nnz_local, rowptr, colind, 0, stream);
+  if (st == GESPMM_OK)
+    st = gespmm_plan_execute(p, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, stream);
+  if (!plan && p) {
+    cudaStreamSynchronize(s);
+    gespmm_plan_destroy(p);
+  }
+  if (st != GESPMM_OK) return st;
+  // 3. optional all-gather of the uneven slabs: one broadcast per owner
+  if (C_full) {
+    r = n.GroupStart();
+    if (r != 0) return nccl_fail(r, "ncclGroupStart");
+    for (int w = 0; w < world; ++w) {
+      const int64_t rows = row_bounds[w + 1] - row_bounds[w];
+      if (rows <= 0) continue;
+      float* recv = C_full + row_bounds[w] * N;
+      const float* send = (w == rank) ? C : recv;
+      r = n.Broadcast(send, recv, static_cast<size_t>(rows * N) * sizeof(float), kNcclChar, w, comm, s);
+      if (r != 0) {
+        n.GroupEnd();
+        return nccl_fail(r, "ncclBroadcast(C slab)");
+      }
+    }
+    r = n.GroupEnd();
+    if (r != 0) return nccl_fail(r, "ncclGroupEnd");
+  }
+  return GESPMM_OK;
+}
+
+}  // extern "C"

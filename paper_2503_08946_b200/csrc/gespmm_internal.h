@@ -1,0 +1,82 @@
+// gespmm_internal.h -- shared between the plan builder, the SpMM kernels and
+// the C-ABI layer.  Not part of the public boundary (include/gespmm.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "gespmm.h"
+
+namespace gespmm {
+
+// ---- work decomposition constants ------------------------
+// Long rows (deg > kSeg) are cut into kSeg-long segments from the row start.
+constexpr int kSeg = GESPMM_SEGMENT_LEN;
+// A tile is a run of consecutive short rows worth ~kTileWork work units, where a
+// row costs deg + kRowCost (the row cost accounts for its C-row store).
+constexpr int kTileWork = 256;
+constexpr int kRowCost = 2;
+// Rows per tile are bounded: every short row advances the work prefix by >= kRowCost.
+constexpr int kTileMaxRows = kTileWork / kRowCost;
+// Kernel geometry: one warp per work item, 8 warps per CTA.
+constexpr int kWarpsPerBlock = 8;
+// Nonzeros staged per warp refill: 32 lanes x one 128-bit colind/vals load each.
+constexpr int kChunk = 128;
+// Low 40 bits of the packed plan scan carry tile work, high 24 bits segment counts.
+constexpr int kPackShift = 40;
+
+// Kernel variant: VEC fp32 columns per lane per load (1, 2 or 4) and CWM column
+// tiles per warp (Coarse-grained Warp Merging); one warp covers 32*VEC*CWM
+// columns of one column block.
+struct Variant {
+  int vec = 1;
+  int cwm = 1;
+};
+
+// Everything the SpMM kernel reads.  Passed by value (kernel parameter space).
+struct KParams {
+  const int* rowptr;
+  const int* colind;
+  const float* vals;
+  const float* B;
+  float* C;
+  int64_t ldb, ldc, N;
+  int64_t ldp;             // leading dimension of the long-row partials
+  const int4* items;       // {row, seg (-1 = tile), rowptr[row], slot base}
+  int64_t n_items;
+  int M;
+  int nnz;
+  float* partials;         // [n_segments][ldp]
+  int* counters;           // [n_segments][ncb], zero between launches
+  int accumulate;
+  int ncb;                 // column blocks (gridDim.y)
+  int idx_aligned;         // colind and vals 16-byte aligned -> 128-bit staging loads
+};
+
+void set_error(const std::string& msg);
+gespmm_status_t fail(gespmm_status_t s, const std::string& msg);
+gespmm_status_t cuda_fail(cudaError_t e, const char* what);
+
+Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc);
+int variant_cols(const Variant& v);
+std::string variant_name(const Variant& v);
+bool parse_variant(const char* name, Variant* v);
+
+cudaError_t launch_spmm(gespmm_reduce_t op, const Variant& v, const KParams& p,
+                        cudaStream_t stream);
+
+}  // namespace gespmm
+
+// Plan object behind the opaque gespmm_plan_t.
+struct gespmm_plan_s {
+  int64_t M = 0, K = 0, nnz = 0;
+  int4* items = nullptr;
+  int64_t n_items = 0, n_tiles = 0, n_long = 0, n_segs = 0;
+  float* partials = nullptr;
+  int64_t partial_floats = 0;
+  int* counters = nullptr;
+  int64_t counter_ints = 0;
+  int device = 0;
+};

@@ -1,0 +1,232 @@
+// gespmm_plan.cu -- nnz-balanced work decomposition, built on the GPU
+// (BASELINE.json north star item (2): "nnz-balanced row-partitioner with a
+// power-law/long-row split path").
+//
+// Input: rowptr of one CSR (plus colind for optional validation).
+// Output: a list of work items, one warp each, in row order:
+//   TILE    {r0, -1, rowptr[r0], 0}: consecutive short rows (deg <= kSeg); the
+//           tile ends where the next item starts.  A short row costs
+//           w = deg + kRowCost work units; row i joins tile floor(E_i / kTileWork)
+//           where E is the exclusive prefix of w, so a tile holds ~kTileWork
+//           units (<= kTileWork + kSeg + kRowCost) and <= kTileMaxRows rows.
+//   SEGMENT {row, s, rowptr[row], slot}: nonzeros [rs + s*kSeg, rs + (s+1)*kSeg)
+//           of a long row; `slot` is the row's first partial-buffer slot.
+// A long row always ends the tile before it.  The decomposition depends only
+// on rowptr -- never on the device or grid -- which is what makes results
+// reproducible across GPUs and across row-sharding.
+//
+// Steps: k_rows (per-row work, packed 40|24-bit, + CSR validation)
+//        -> exclusive scan (CUB) -> k_count (items per row) -> exclusive scan
+//        -> one D2H of the totals (the only host sync) -> k_emit.
+// The reference validates the same CSR rules on the host (src/oracle.cpp:291-316).
+#include <cub/device/device_scan.cuh>
+
+#include <cstdio>
+
+#include "gespmm_internal.h"
+
+namespace gespmm {
+namespace {
+
+constexpr uint64_t kLowMask = (uint64_t(1) << kPackShift) - 1;
+
+enum : int { kErrRowptr0 = 1, kErrMonotone = 2, kErrEnd = 4, kErrColRange = 8 };
+
+__global__ void k_rows(const int* __restrict__ rowptr, int M, int nnz,
+                       uint64_t* __restrict__ packed, int* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const int a = rowptr[i];
+  const int b = rowptr[i + 1];
+  int e = 0;
+  if (i == 0 && a != 0) e |= kErrRowptr0;
+  if (b < a) e |= kErrMonotone;
+  if (i == M - 1 && b != nnz) e |= kErrEnd;
+  if (e) atomicOr(err, e);
+  const int deg = b >= a ? b - a : 0;
+  const bool lng = deg > kSeg;
+  if (lng) atomicAdd(err + 1, 1);  // long-row count (plan info)
+  const uint64_t w = lng ? 0 : static_cast<uint64_t>(deg + kRowCost);
+  const uint64_t ns = lng ? static_cast<uint64_t>((deg + kSeg - 1) / kSeg) : 0;
+  packed[i] = (ns << kPackShift) | w;
+}
+
+__global__ void k_colind(const int* __restrict__ colind, int64_t nnz, int K, int* __restrict__ err) {
+  int bad = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz; p += stride) {
+    const int c = __ldcs(colind + p);
+    bad |= (c < 0) | (c >= K);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrColRange);
+}
+
+__device__ __forceinline__ bool tile_start(int i, const uint64_t* packed, const uint64_t* E) {
+  const uint64_t pi = packed[i];
+  if ((pi & kLowMask) == 0) return false;  // long row: no tile starts here
+  if (i == 0) return true;
+  const uint64_t pp = packed[i - 1];
+  if ((pp & kLowMask) == 0) return true;   // previous row is long
+  return ((E[i] & kLowMask) / kTileWork) != ((E[i - 1] & kLowMask) / kTileWork);
+}
+
+__global__ void k_count(const uint64_t* __restrict__ packed, const uint64_t* __restrict__ E, int M,
+                        int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  cnt[i] = (tile_start(i, packed, E) ? 1 : 0) + static_cast<int>(packed[i] >> kPackShift);
+}
+
+__global__ void k_emit(const int* __restrict__ rowptr, const uint64_t* __restrict__ packed,
+                       const uint64_t* __restrict__ E, const int* __restrict__ pos, int M,
+                       int4* __restrict__ items) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  int p = pos[i];
+  const int rs = rowptr[i];
+  if (tile_start(i, packed, E)) items[p++] = make_int4(i, -1, rs, 0);
+  const int ns = static_cast<int>(packed[i] >> kPackShift);
+  const int slot = static_cast<int>(E[i] >> kPackShift);
+  for (int s = 0; s < ns; ++s) items[p++] = make_int4(i, s, rs, slot);
+}
+
+struct Totals {
+  uint64_t last_packed;
+  uint64_t last_E;
+  int last_cnt;
+  int last_pos;
+  int err;
+  int n_long;
+};
+
+__global__ void k_totals(const uint64_t* packed, const uint64_t* E, const int* cnt, const int* pos,
+                         int M, const int* err, Totals* out) {
+  out->last_packed = packed[M - 1];
+  out->last_E = E[M - 1];
+  out->last_cnt = cnt[M - 1];
+  out->last_pos = pos[M - 1];
+  out->err = err[0];
+  out->n_long = err[1];
+}
+
+std::string csr_error_text(int err, int64_t K) {
+  // wording follows raceset::validate_instance (src/oracle.cpp:302-315)
+  if (err & kErrRowptr0) return "invalid csr: rowPtr[0] must be 0";
+  if (err & kErrMonotone) return "invalid csr: rowPtr must be nondecreasing";
+  if (err & kErrEnd) return "invalid csr: rowPtr end differs from nnz of colInd";
+  if (err & kErrColRange) return "invalid csr: colInd entry out of [0," + std::to_string(K) + ")";
+  return "invalid csr";
+}
+
+}  // namespace
+
+// Validates colind on the device; returns the error bits via *err_host (sync).
+gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K,
+                                       cudaStream_t s) {
+  int* err = nullptr;
+  cudaError_t ce = cudaMallocAsync(&err, sizeof(int), s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMallocAsync");
+  cudaMemsetAsync(err, 0, sizeof(int), s);
+  if (nnz > 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (nnz + 255) / 256;
+    if (blocks > 4 * sms) blocks = 4 * sms;
+    k_colind<<<static_cast<unsigned>(blocks), 256, 0, s>>>(colind, nnz, static_cast<int>(K), err);
+  }
+  int h = 0;
+  cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(err, s);
+  ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "validate colind");
+  if (h) return fail(GESPMM_CSR_INVALID, csr_error_text(h, K));
+  return GESPMM_OK;
+}
+
+gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* colind,
+                           bool check_colind, cudaStream_t s) {
+  const int64_t M = plan->M;
+  const int M32 = static_cast<int>(M);
+  const int nnz32 = static_cast<int>(plan->nnz);
+  cudaError_t ce;
+  if (M == 0) {
+    plan->n_items = plan->n_tiles = plan->n_long = plan->n_segs = 0;
+    if (plan->nnz != 0) return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr end differs from nnz of colInd");
+    return GESPMM_OK;
+  }
+  // temporaries (stream-ordered)
+  uint64_t *packed = nullptr, *E = nullptr;
+  int *cnt = nullptr, *pos = nullptr, *err = nullptr;
+  Totals* tot = nullptr;
+  void* tmp = nullptr;
+  size_t tmp1 = 0, tmp2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp1, packed, E, M32, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, cnt, pos, M32, s);
+  const size_t tmp_bytes = tmp1 > tmp2 ? tmp1 : tmp2;
+  const size_t bytes = M * (8 + 8 + 4 + 4) + 64 + sizeof(Totals) + tmp_bytes + 8 * 256;
+  char* arena = nullptr;
+  ce = cudaMallocAsync(&arena, bytes, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "plan temporaries");
+  {
+    char* p = arena;
+    auto take = [&](size_t n) {
+      char* r = p;
+      p += (n + 255) & ~size_t(255);
+      return r;
+    };
+    packed = reinterpret_cast<uint64_t*>(take(M * 8));
+    E = reinterpret_cast<uint64_t*>(take(M * 8));
+    cnt = reinterpret_cast<int*>(take(M * 4));
+    pos = reinterpret_cast<int*>(take(M * 4));
+    err = reinterpret_cast<int*>(take(64));
+    tot = reinterpret_cast<Totals*>(take(sizeof(Totals)));
+    tmp = take(tmp_bytes);
+    (void)bytes;
+  }
+  const unsigned blocks = static_cast<unsigned>((M + 255) / 256);
+  cudaMemsetAsync(err, 0, 2 * sizeof(int), s);
+  k_rows<<<blocks, 256, 0, s>>>(rowptr, M32, nnz32, packed, err);
+  if (check_colind && plan->nnz > 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t cblocks = (plan->nnz + 255) / 256;
+    if (cblocks > 4 * sms) cblocks = 4 * sms;
+    k_colind<<<static_cast<unsigned>(cblocks), 256, 0, s>>>(colind, plan->nnz,
+                                                            static_cast<int>(plan->K), err);
+  }
+  size_t tb = tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, packed, E, M32, s);
+  k_count<<<blocks, 256, 0, s>>>(packed, E, M32, cnt);
+  tb = tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pos, M32, s);
+  k_totals<<<1, 1, 0, s>>>(packed, E, cnt, pos, M32, err, tot);
+  Totals h{};
+  cudaMemcpyAsync(&h, tot, sizeof(Totals), cudaMemcpyDeviceToHost, s);
+  ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) {
+    cudaFreeAsync(arena, s);
+    return cuda_fail(ce, "plan build");
+  }
+  if (h.err) {
+    cudaFreeAsync(arena, s);
+    return fail(GESPMM_CSR_INVALID, csr_error_text(h.err, plan->K));
+  }
+  plan->n_items = static_cast<int64_t>(h.last_pos) + h.last_cnt;
+  plan->n_segs = static_cast<int64_t>(h.last_E >> kPackShift) + static_cast<int64_t>(h.last_packed >> kPackShift);
+  plan->n_long = h.n_long;
+  plan->n_tiles = plan->n_items - plan->n_segs;
+  ce = cudaMalloc(&plan->items, static_cast<size_t>(plan->n_items > 0 ? plan->n_items : 1) * sizeof(int4));
+  if (ce != cudaSuccess) {
+    cudaFreeAsync(arena, s);
+    return cuda_fail(ce, "plan items");
+  }
+  k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, plan->items);
+  ce = cudaGetLastError();
+  cudaFreeAsync(arena, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "plan emit");
+  return GESPMM_OK;
+}
+
+}  // namespace gespmm

@@ -1,0 +1,217 @@
+"""Public SpMM API on torch CUDA tensors (PyTorch = device memory + streams only;
+all compute is libgespmm.so's sm_100a kernels through the C-ABI).
+
+    C = csr_spmm(rowptr, colind, vals, B, reduce="sum")            # one-shot
+    plan = Plan(rowptr, colind, K)                                   # reusable
+    plan.execute(vals, B, reduce="max", out=C)                       # async
+
+Reference surface this mirrors: the kernel
+``@gespmm_alg2(%rowPtr, %colInd, %val, %B, %C, %M, %N, %K)``
+(/root/reference/proj/fixtures/gespmm_alg2.mir:5) run through
+``raceset::run`` (src/oracle.cpp:699-736), with the CSR contract of
+``validate_instance`` (src/oracle.cpp:291-316).  ``accumulate=True`` is the
+reference kernel's read-modify-write of C (gespmm_alg2.mir:55-59); the
+default writes C = A (op) B.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import Error, ErrorKind
+
+_L = _lib.load()  # no library, no API (no CPU fallback)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_handle(stream, device):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _reduce_code(reduce) -> int:
+    if isinstance(reduce, int):
+        return reduce
+    try:
+        return _lib.REDUCE[reduce]
+    except KeyError:
+        raise Error(ErrorKind.InvalidArgument, f"unknown reduce op {reduce!r}") from None
+
+
+def _check_csr_tensors(rowptr, colind, vals):
+    torch = _torch()
+    for name, t, dt in (("rowptr", rowptr, torch.int32), ("colind", colind, torch.int32)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise Error(ErrorKind.InvalidArgument, f"{name} must be a contiguous int32 CUDA tensor")
+    if vals is not None and (vals.dtype != torch.float32 or not vals.is_cuda or
+                             not vals.is_contiguous()):
+        raise Error(ErrorKind.InvalidArgument, "vals must be a contiguous float32 CUDA tensor")
+    if vals is not None and vals.numel() != colind.numel():
+        raise Error(ErrorKind.CsrInvalid, "colInd and val lengths differ")
+
+
+def _check_dense(name, t):
+    torch = _torch()
+    if t.dtype != torch.float32 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+        raise Error(ErrorKind.InvalidArgument,
+                    f"{name} must be a 2-D float32 CUDA tensor with unit column stride")
+
+
+class Plan:
+    """The nnz-balanced work decomposition of one sparsity structure
+    (gespmm_plan_create).  Reusable for any vals / B / N / reduce op."""
+
+    def __init__(self, rowptr, colind, K: int, validate: bool = True, stream=None):
+        _check_csr_tensors(rowptr, colind, None)
+        self.M = rowptr.numel() - 1
+        self.K = int(K)
+        self.nnz = colind.numel()
+        self.rowptr = rowptr
+        self.colind = colind
+        self.device = rowptr.device
+        h = ctypes.c_void_p()
+        _lib.check(_L.gespmm_plan_create(ctypes.byref(h), self.M, self.K, self.nnz,
+                                         rowptr.data_ptr(), colind.data_ptr(),
+                                         1 if validate else 0,
+                                         _stream_handle(stream, self.device)))
+        self._h = h
+
+    def info(self) -> dict:
+        inf = _lib.PlanInfo()
+        _lib.check(_L.gespmm_plan_get_info(self._h, ctypes.byref(inf)))
+        return {n: getattr(inf, n) for n, _ in _lib.PlanInfo._fields_}
+
+    def execute(self, vals, B, reduce="sum", out=None, accumulate: bool = False, stream=None):
+        torch = _torch()
+        _check_csr_tensors(self.rowptr, self.colind, vals)
+        _check_dense("B", B)
+        if B.shape[0] != self.K:
+            raise Error(ErrorKind.InvalidArgument, f"B has {B.shape[0]} rows, expected K={self.K}")
+        N = B.shape[1]
+        if out is None:
+            if accumulate:
+                raise Error(ErrorKind.InvalidArgument, "accumulate=True needs out (C0)")
+            out = torch.empty((self.M, N), dtype=torch.float32, device=B.device)
+        _check_dense("out", out)
+        if tuple(out.shape) != (self.M, N):
+            raise Error(ErrorKind.InvalidArgument, f"out must be {(self.M, N)}")
+        _lib.check(_L.gespmm_plan_execute(
+            self._h, N, self.rowptr.data_ptr(), self.colind.data_ptr(), vals.data_ptr(),
+            B.data_ptr(), B.stride(0), out.data_ptr(), out.stride(0), _reduce_code(reduce),
+            1 if accumulate else 0, _stream_handle(stream, B.device)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _L.gespmm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def csr_spmm(rowptr, colind, vals, B, reduce="sum", out=None, accumulate: bool = False,
+             stream=None):
+    """One-shot C = A (reduce) B on CUDA tensors (gespmm_csr_spmm): validates the
+    CSR on the device, plans, launches."""
+    torch = _torch()
+    _check_csr_tensors(rowptr, colind, vals)
+    _check_dense("B", B)
+    M, K, N = rowptr.numel() - 1, B.shape[0], B.shape[1]
+    if out is None:
+        if accumulate:
+            raise Error(ErrorKind.InvalidArgument, "accumulate=True needs out (C0)")
+        out = torch.empty((M, N), dtype=torch.float32, device=B.device)
+    _check_dense("out", out)
+    _lib.check(_L.gespmm_csr_spmm(M, K, N, colind.numel(), rowptr.data_ptr(), colind.data_ptr(),
+                                  vals.data_ptr(), B.data_ptr(), B.stride(0), out.data_ptr(),
+                                  out.stride(0), _reduce_code(reduce), 1 if accumulate else 0,
+                                  _stream_handle(stream, B.device)))
+    return out
+
+
+def _np(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def csr_spmm_host(rowptr, colind, vals, B, reduce="sum", C0=None, out=None):
+    """One-shot SpMM on HOST (numpy or pinned torch CPU) buffers through
+    gespmm_csr_spmm_host: H2D, device validation, plan, kernel, D2H."""
+    torch = _torch()
+
+    def ptr(a):
+        if isinstance(a, torch.Tensor):
+            return a.data_ptr()
+        return a.ctypes.data
+
+    if not isinstance(rowptr, torch.Tensor):
+        rowptr = _np(rowptr, np.int32)
+        colind = _np(colind, np.int32)
+        vals = _np(vals, np.float32)
+        B = _np(B, np.float32)
+    M = rowptr.shape[0] - 1
+    K, N = B.shape
+    accumulate = C0 is not None
+    if out is None:
+        if isinstance(B, torch.Tensor):
+            out = torch.empty((M, N), dtype=torch.float32, pin_memory=B.is_pinned())
+        else:
+            out = np.zeros((M, N), np.float32)
+    if accumulate:
+        if isinstance(out, torch.Tensor):
+            out.copy_(torch.as_tensor(C0))
+        else:
+            out[...] = C0
+    _lib.check(_L.gespmm_csr_spmm_host(M, K, N, colind.shape[0], ptr(rowptr), ptr(colind),
+                                       ptr(vals), ptr(B), N, ptr(out), N, _reduce_code(reduce),
+                                       1 if accumulate else 0, None))
+    return out
+
+
+def validate_csr(M: int, K: int, rowptr, colind, vals_len=None) -> None:
+    """Host CSR validation with the reference's rules (raises Error(CsrInvalid))."""
+    rp = _np(rowptr, np.int32)
+    ci = _np(colind, np.int32)
+    n = ci.shape[0] if vals_len is None else int(vals_len)
+    _lib.check(_L.gespmm_validate_csr(M, K, rp.shape[0], rp.ctypes.data, ci.shape[0],
+                                      ci.ctypes.data, n))
+
+
+def validate_csr_device(rowptr, colind, K: int, stream=None) -> None:
+    _check_csr_tensors(rowptr, colind, None)
+    _lib.check(_L.gespmm_validate_csr_device(rowptr.numel() - 1, K, colind.numel(),
+                                             rowptr.data_ptr(), colind.data_ptr(),
+                                             _stream_handle(stream, rowptr.device)))
+
+
+def partition_rows(rowptr, parts: int) -> np.ndarray:
+    """nnz(+rows)-balanced contiguous row blocks for `parts` ranks (host)."""
+    rp = _np(rowptr, np.int32)
+    bounds = np.zeros(parts + 1, np.int64)
+    _lib.check(_L.gespmm_partition_rows(rp.shape[0] - 1, rp.ctypes.data, parts,
+                                        bounds.ctypes.data))
+    return bounds
+
+
+def variant_name(N: int, B=None, out=None) -> str:
+    bp = B.data_ptr() if B is not None else 0
+    cp = out.data_ptr() if out is not None else 0
+    ldb = B.stride(0) if B is not None else N
+    ldc = out.stride(0) if out is not None else N
+    return _L.gespmm_variant_name(N, bp, ldb, cp, ldc).decode()
+
+
+def set_variant_override(name: str = "") -> None:
+    _lib.check(_L.gespmm_set_variant_override(name.encode()))

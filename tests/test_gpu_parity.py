@@ -1,0 +1,323 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the oracle.
+
+Bar (BASELINE.json north star): sum/mean within 1e-5 norm-wise of the fp64
+reference; and -- stronger -- bit-identical to the fp32 twin
+(oracle/gespmm_oracle.c) for every op, every kernel variant, split and
+unsplit rows.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+SEG = 256
+OPS = ["sum", "max", "min", "mean"]
+VARIANTS = ["vec1_lpr32_cwm1", "vec1_lpr32_cwm2", "vec2_lpr32_cwm1", "vec2_lpr32_cwm2",
+            "vec4_lpr32_cwm1", "vec4_lpr32_cwm2"]
+
+
+def to_dev(cuda, *arrs):
+    import torch
+
+    return [torch.as_tensor(np.ascontiguousarray(a), device=cuda) for a in arrs]
+
+
+def random_csr(rng, M, K, density, long_rows=(), dup=False, empty_frac=0.0):
+    rows = []
+    for i in range(M):
+        d = rng.binomial(K, density)
+        if rng.random() < empty_frac:
+            d = 0
+        for (r, dd) in long_rows:
+            if r == i:
+                d = dd
+        c = rng.integers(0, K, d) if (dup or d > K) else np.sort(rng.choice(K, d, replace=False))
+        rows.append(c)
+    rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)
+    colind = np.concatenate(rows).astype(np.int32) if rows else np.zeros(0, np.int32)
+    vals = rng.uniform(-1, 1, colind.size).astype(np.float32)
+    return rowptr, colind, vals
+
+
+def gpu_spmm(cuda, rowptr, colind, vals, B, op, C0=None, K=None):
+    import torch
+
+    from paper_2503_08946_b200.spmm import Plan
+
+    rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, vals, B)
+    K = B.shape[0] if K is None else K
+    plan = Plan(rp, ci, K)
+    if C0 is not None:
+        out = torch.as_tensor(C0.copy(), device=cuda)
+        plan.execute(vv, Bt, reduce=op, out=out, accumulate=True)
+    else:
+        out = plan.execute(vv, Bt, reduce=op)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), plan
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_golden_instances_via_reference_interface(cuda, name):
+    """run(inst) with the reference's launch semantics vs the reference's own C."""
+    from paper_2503_08946_b200 import instance as I
+
+    g = load_golden(name)
+    M, N, K = g["M"], g["N"], g["K"]
+    inst = I.ConcreteInstance(
+        name=name, params={"M": M, "N": N, "K": K, "A_S": len(g["colind"])},
+        arrays={"rowPtr": I.ArrayData("i32", ints=g["rowptr"]),
+                "colInd": I.ArrayData("i32", ints=g["colind"]),
+                "val": I.ArrayData("f32", floats=g["vals"]),
+                "B": I.ArrayData("f32", floats=g["B"]),
+                "C": I.ArrayData("f32", floats=g["C0"])},
+        grid=g["grid"], block=g["block"], csr=I.CsrSpec("rowPtr", "colInd", "val", K))
+    C = I.run(inst).astype(np.float64)
+    ref = np.asarray(g["C"], np.float64).reshape(M, N)
+    C0 = np.abs(np.asarray(g["C0"], np.float64).reshape(M, N))
+    rp = np.asarray(g["rowptr"], np.int64)
+    ci = np.asarray(g["colind"], np.int64)
+    v = np.abs(np.asarray(g["vals"], np.float64))
+    Bm = np.abs(np.asarray(g["B"], np.float64).reshape(K, N))
+    bound = np.zeros((M, N))
+    for i in range(M):
+        for p in range(rp[i], rp[i + 1]):
+            bound[i] += v[p] * Bm[ci[p]]
+    tol = 1e-5 * np.maximum(np.abs(ref), bound + C0) + 1e-30
+    assert np.all(np.abs(C - ref) <= tol), np.abs(C - ref).max()
+    if name.startswith("ref_"):
+        np.testing.assert_array_equal(C, ref)  # integer-valued shipped instances: exact
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("N", [1, 4, 12, 16, 32, 64, 100, 128, 256, 264, 512])
+def test_bit_exact_vs_twin(cuda, oracle_mod, op, N):
+    rng = np.random.default_rng(100 + N)
+    M, K = 700, 300
+    rowptr, colind, vals = random_csr(rng, M, K, 0.05, long_rows=[(5, 1000), (6, 257), (699, 2600)],
+                                      dup=True, empty_frac=0.3)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_accumulate_bit_exact(cuda, oracle_mod, op):
+    rng = np.random.default_rng(7)
+    M, K, N = 500, 400, 64
+    rowptr, colind, vals = random_csr(rng, M, K, 0.03, long_rows=[(3, 900)], empty_frac=0.2)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op, C0=C0)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_every_variant_bit_exact(cuda, oracle_mod, variant, op):
+    from paper_2503_08946_b200 import spmm
+
+    rng = np.random.default_rng(11)
+    M, K, N = 900, 500, 96
+    rowptr, colind, vals = random_csr(rng, M, K, 0.04, long_rows=[(10, 3000)], empty_frac=0.4)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    spmm.set_variant_override(variant)
+    try:
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+    finally:
+        spmm.set_variant_override("")
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_max_min_special_values(cuda, oracle_mod):
+    """NaN first/later messages, +-0, +-inf: max/min bit-exact by construction."""
+    rng = np.random.default_rng(5)
+    M, K, N = 300, 64, 32
+    rowptr, colind, vals = random_csr(rng, M, K, 0.2, long_rows=[(1, 600), (2, 700)])
+    vals[::7] = np.nan
+    vals[1::11] = 0.0
+    vals[2::13] = -0.0
+    vals[3::17] = np.inf
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    B[::5] = -0.0
+    B[1::9] = -np.inf
+    for op in ("max", "min", "sum", "mean"):
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_segmented_max_equals_unsegmented(cuda, oracle_mod):
+    """Max/min are independent of the long-row split (proved in DESIGN.md)."""
+    rng = np.random.default_rng(9)
+    rowptr, colind, vals = random_csr(rng, 50, 4000, 0.01, long_rows=[(0, 3999), (7, 513)])
+    B = rng.uniform(-1, 1, (4000, 64)).astype(np.float32)
+    for op in ("max", "min"):
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=0)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_empty_and_degenerate(cuda, oracle_mod):
+    import torch
+
+    from paper_2503_08946_b200.spmm import csr_spmm
+
+    # nnz = 0
+    rowptr = np.zeros(11, np.int32)
+    colind = np.zeros(0, np.int32)
+    vals = np.zeros(0, np.float32)
+    B = np.ones((5, 8), np.float32)
+    for op in OPS:
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        np.testing.assert_array_equal(got, np.zeros((10, 8), np.float32))
+    # M = 0
+    rp, ci, vv, Bt = to_dev(cuda, np.zeros(1, np.int32), colind, vals, B)
+    out = csr_spmm(rp, ci, vv, Bt)
+    assert tuple(out.shape) == (0, 8)
+    # single dense row
+    rowptr = np.array([0, 5], np.int32)
+    colind = np.arange(5, dtype=np.int32)
+    vals = np.arange(1, 6, dtype=np.float32)
+    got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, "sum")
+    np.testing.assert_array_equal(got, np.full((1, 8), 15.0, np.float32))
+    torch.cuda.synchronize()
+
+
+def test_misaligned_views_bit_exact(cuda, oracle_mod):
+    """Offset (non-16B-aligned) colind/vals/B/C force the scalar staging and
+    VEC=1 paths."""
+    import torch
+
+    from paper_2503_08946_b200.spmm import Plan
+
+    rng = np.random.default_rng(21)
+    M, K, N = 400, 300, 64
+    rowptr, colind, vals = random_csr(rng, M, K, 0.05, long_rows=[(4, 800)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    ci_big = torch.zeros(colind.size + 1, dtype=torch.int32, device=cuda)
+    ci_big[1:] = torch.as_tensor(colind, device=cuda)
+    v_big = torch.zeros(vals.size + 1, dtype=torch.float32, device=cuda)
+    v_big[1:] = torch.as_tensor(vals, device=cuda)
+    B_big = torch.zeros(K * N + 1, dtype=torch.float32, device=cuda)
+    B_big[1:] = torch.as_tensor(B.ravel(), device=cuda)
+    Bt = B_big[1:].view(K, N)
+    C_big = torch.zeros(M * N + 1, dtype=torch.float32, device=cuda)
+    out = C_big[1:].view(M, N)
+    rp = torch.as_tensor(rowptr, device=cuda)
+    plan = Plan(rp, ci_big[1:], K)
+    plan.execute(v_big[1:], Bt, reduce="sum", out=out)
+    torch.cuda.synchronize()
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG)
+    np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def test_strided_B_and_C(cuda, oracle_mod):
+    import torch
+
+    from paper_2503_08946_b200.spmm import Plan
+
+    rng = np.random.default_rng(3)
+    M, K, N = 300, 200, 64
+    rowptr, colind, vals = random_csr(rng, M, K, 0.05)
+    Bw = rng.uniform(-1, 1, (K, N + 8)).astype(np.float32)
+    rp, ci, vv = to_dev(cuda, rowptr, colind, vals)
+    Bt = torch.as_tensor(Bw, device=cuda)[:, :N]
+    outw = torch.full((M, N + 4), 7.0, device=cuda)
+    plan = Plan(rp, ci, K)
+    plan.execute(vv, Bt, reduce="sum", out=outw[:, :N])
+    torch.cuda.synchronize()
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, np.ascontiguousarray(Bw[:, :N]), "sum",
+                               seg_len=SEG)
+    np.testing.assert_array_equal(outw[:, :N].cpu().numpy(), want)
+    assert torch.all(outw[:, N:] == 7.0)
+
+
+def test_invalid_csr_raises_like_reference(cuda):
+    from paper_2503_08946_b200 import Error, ErrorKind
+    from paper_2503_08946_b200.spmm import csr_spmm
+
+    B = np.ones((2, 4), np.float32)
+    bad = [  # (rowptr, colind, message) -- reference src/oracle.cpp:302-315 wording
+        (np.array([0, 2, 1], np.int32), np.array([0, 0], np.int32), "nondecreasing"),
+        (np.array([1, 2, 2], np.int32), np.array([0, 0], np.int32), "[0] must be 0"),
+        (np.array([0, 1, 3], np.int32), np.array([0, 1], np.int32), "end differs"),
+        (np.array([0, 1, 2], np.int32), np.array([0, 2], np.int32), "out of [0,2)"),
+    ]
+    for rowptr, colind, msg in bad:
+        rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, np.ones(colind.size, np.float32), B)
+        with pytest.raises(Error) as ei:
+            csr_spmm(rp, ci, vv, Bt)
+        assert ei.value.kind == ErrorKind.CsrInvalid
+        assert msg in str(ei.value)
+
+
+def test_host_entry_point(cuda, oracle_mod):
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    rng = np.random.default_rng(4)
+    M, K, N = 1000, 800, 32
+    rowptr, colind, vals = random_csr(rng, M, K, 0.02, long_rows=[(2, 700)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, "mean")
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "mean", seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, "sum", C0=C0)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", accumulate=True, C0=C0, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_deterministic_and_shard_invariant(cuda, oracle_mod):
+    """Same bits run-to-run, and row-sharded computation (the multi-GPU path's
+    per-rank work) reproduces the unsharded result bit for bit."""
+    import torch
+
+    from paper_2503_08946_b200 import workloads as W
+    from paper_2503_08946_b200.spmm import Plan, partition_rows
+
+    csr = W.rmat_csr(14, 200_000, seed=3, device=cuda)
+    M, K, N = csr.M, csr.K, 64
+    B = W.dense_torch(K, N, seed=2, device=cuda)
+    plan = Plan(csr.rowptr, csr.colind, K)
+    c1 = plan.execute(csr.vals, B, "sum").clone()
+    c2 = plan.execute(csr.vals, B, "sum").clone()
+    assert torch.equal(c1, c2)
+    rp_h = csr.rowptr.cpu().numpy()
+    for parts in (2, 4, 8):
+        bounds = partition_rows(rp_h, parts)
+        full = torch.empty_like(c1)
+        for r in range(parts):
+            a, b = int(bounds[r]), int(bounds[r + 1])
+            p0, p1 = int(rp_h[a]), int(rp_h[b])
+            rp = (csr.rowptr[a:b + 1] - p0).contiguous()
+            sp = Plan(rp, csr.colind[p0:p1].contiguous(), K)
+            sp.execute(csr.vals[p0:p1].contiguous(), B, "sum", out=full[a:b])
+        torch.cuda.synchronize()
+        assert torch.equal(full, c1)
+    want = oracle_mod.spmm_f32(rp_h, csr.colind.cpu().numpy(), csr.vals.cpu().numpy(),
+                               B.cpu().numpy(), "sum", seg_len=SEG)
+    np.testing.assert_array_equal(c1.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_config2_full_size_bit_exact(cuda, oracle_mod, op):
+    """BASELINE config 2 (R-MAT scale 20, 16M edges, N=64) at full size: GPU
+    equals the twin bit for bit (the twin runs on all host cores)."""
+    import torch
+
+    from paper_2503_08946_b200 import workloads as W
+    from paper_2503_08946_b200.spmm import Plan
+
+    csr = W.rmat_csr(20, 16 * 2**20, seed=3, device=cuda)
+    B = W.dense_torch(csr.K, 64, seed=2, device=cuda)
+    plan = Plan(csr.rowptr, csr.colind, csr.K)
+    got = plan.execute(csr.vals, B, op)
+    torch.cuda.synchronize()
+    want = oracle_mod.spmm_f32(csr.rowptr.cpu().numpy(), csr.colind.cpu().numpy(),
+                               csr.vals.cpu().numpy(), B.cpu().numpy(), op, seg_len=SEG)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
