@@ -20,6 +20,13 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libgespmm.so")
+# Experiment builds: GESPMM_BUILD_TAG=mb3 GESPMM_EXTRA_FLAGS="-DGESPMM_MINBLOCKS=3"
+# -> libgespmm_mb3.so (selected at run time with GESPMM_LIB=...).
+TAG = os.environ.get("GESPMM_BUILD_TAG", "")
+EXTRA = os.environ.get("GESPMM_EXTRA_FLAGS", "").split()
+if TAG:
+    LIB = os.path.join(PKG, f"libgespmm_{TAG}.so")
+    BUILD = os.path.join(PKG, f"build_{TAG}")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,7 +49,7 @@ def _compile(src: str, verbose: bool) -> str:
     newest_dep = max(os.path.getmtime(p) for p in [src] + _headers())
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", src, "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

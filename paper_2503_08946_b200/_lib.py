@@ -12,7 +12,7 @@ import os
 from .errors import Error, ErrorKind
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgespmm.so")
+LIB_PATH = os.environ.get("GESPMM_LIB") or os.path.join(PKG, "libgespmm.so")
 
 OK, CSR_INVALID, OUT_OF_BOUNDS, INVALID_ARG, CUDA_ERROR, NCCL_ERROR, NOT_SUPPORTED = range(7)
 REDUCE = {"sum": 0, "max": 1, "min": 2, "mean": 3}

@@ -218,6 +218,7 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
   p.ncb = ncb;
   p.idx_aligned = (reinterpret_cast<uintptr_t>(colind) % 16 == 0) &&
                   (reinterpret_cast<uintptr_t>(vals) % 16 == 0);
+  p.off32 = plan->K * ldb <= (int64_t(1) << 32);
   cudaError_t e = launch_spmm(op, v, p, s);
   if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
   return GESPMM_OK;

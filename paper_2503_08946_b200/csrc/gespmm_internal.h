@@ -53,6 +53,7 @@ struct KParams {
   int accumulate;
   int ncb;                 // column blocks (gridDim.y)
   int idx_aligned;         // colind and vals 16-byte aligned -> 128-bit staging loads
+  int off32;               // K*ldb <= 2^32: stage 32-bit B-row element offsets
 };
 
 void set_error(const std::string& msg);

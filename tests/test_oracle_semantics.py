@@ -1,0 +1,127 @@
+"""CPU tier: the fp32 twin (the normative semantics the GPU is bit-exact to)
+checked against a pure-Python restatement on small cases, plus the algebraic
+properties DESIGN.md relies on (segmentation invariance of max/min, mean =
+sum/deg, accumulate = the reference's C read-modify-write order)."""
+import math
+
+import numpy as np
+import pytest
+
+SEG = 256
+
+
+def py_twin(rowptr, colind, vals, B, op, accumulate=False, C0=None, seg=0):
+    """Pure-Python fp32 restatement (np.float32 scalars; fma via exact fp64
+    product + single rounding, valid since an fp32*fp32 product is exact in
+    fp64 and fp64 add then fp32 round is NOT an fma -- so use math.fma)."""
+    f32 = np.float32
+    M, N = len(rowptr) - 1, B.shape[1]
+    C = np.zeros((M, N), np.float32) if C0 is None else C0.astype(np.float32).copy()
+    for i in range(M):
+        rs, re = int(rowptr[i]), int(rowptr[i + 1])
+        deg = re - rs
+        segs = [(rs, re)] if (seg <= 0 or deg <= seg) else [(s, min(s + seg, re)) for s in range(rs, re, seg)]
+        for j in range(N):
+            c0 = f32(C[i, j]) if accumulate else f32(0)
+            if op in ("sum", "mean"):
+                acc_total = None
+                for k, (a, b) in enumerate(segs):
+                    acc = c0 if (k == 0 and accumulate and op == "sum") else f32(0)
+                    for p in range(a, b):
+                        acc = f32(math.fma(float(vals[p]), float(B[colind[p], j]), float(acc)))
+                    acc_total = acc if acc_total is None else f32(acc_total + acc)
+                if acc_total is None:
+                    acc_total = c0 if (accumulate and op == "sum") else f32(0)
+                if op == "mean":
+                    r = f32(acc_total / f32(deg)) if deg else f32(0)
+                    C[i, j] = f32(c0 + r) if accumulate else r
+                else:
+                    C[i, j] = acc_total
+            else:
+                better = (lambda m, a: m if m > a else a) if op == "max" else (lambda m, a: m if m < a else a)
+                if deg == 0:
+                    C[i, j] = c0 if accumulate else f32(0)
+                    continue
+                acc = None
+                for k, (a, b) in enumerate(segs):
+                    if k == 0:
+                        part = c0 if accumulate else None
+                    else:
+                        part = f32(-np.inf) if op == "max" else f32(np.inf)
+                    for p in range(a, b):
+                        m = f32(vals[p] * B[colind[p], j])
+                        part = m if part is None else better(m, part)
+                    acc = part if acc is None else better(part, acc)
+                C[i, j] = acc
+    return C
+
+
+def rand_case(seed, M=40, K=30, N=5, long_deg=0, special=False):
+    rng = np.random.default_rng(seed)
+    deg = rng.integers(0, 8, M)
+    deg[rng.random(M) < 0.25] = 0
+    if long_deg:
+        deg[3] = long_deg
+    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    colind = rng.integers(0, K, int(rowptr[-1])).astype(np.int32)
+    vals = rng.uniform(-1, 1, colind.size).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    if special:
+        vals[::5] = np.nan
+        vals[1::7] = -0.0
+        B[::3] = -0.0
+        B[1::4] = np.inf
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    return rowptr, colind, vals, B, C0
+
+
+@pytest.mark.parametrize("op", ["sum", "max", "min", "mean"])
+@pytest.mark.parametrize("accumulate", [False, True])
+@pytest.mark.parametrize("special", [False, True])
+def test_twin_matches_python_restatement(oracle_mod, op, accumulate, special):
+    rowptr, colind, vals, B, C0 = rand_case(1, long_deg=40, special=special)
+    for seg in (0, 16):
+        want = py_twin(rowptr, colind, vals, B, op, accumulate, C0 if accumulate else None, seg)
+        got = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=accumulate,
+                                  C0=C0 if accumulate else None, seg_len=seg)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("op", ["max", "min"])
+@pytest.mark.parametrize("seg", [1, 3, 16, 256])
+def test_max_min_independent_of_segmentation(oracle_mod, op, seg):
+    for special in (False, True):
+        rowptr, colind, vals, B, C0 = rand_case(7, M=60, K=50, N=9, long_deg=700, special=special)
+        for acc in (False, True):
+            a = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=acc, C0=C0, seg_len=0)
+            b = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=acc, C0=C0, seg_len=seg)
+            np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_mean_is_sum_over_degree(oracle_mod):
+    rowptr, colind, vals, B, _ = rand_case(3, long_deg=600)
+    s = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG)
+    m = oracle_mod.spmm_f32(rowptr, colind, vals, B, "mean", seg_len=SEG)
+    deg = np.diff(rowptr).astype(np.float32)[:, None]
+    want = np.where(deg > 0, s / np.where(deg > 0, deg, 1), 0).astype(np.float32)
+    np.testing.assert_array_equal(m, want)
+
+
+def test_accumulate_sum_seeds_chain_with_c0(oracle_mod):
+    """accumulate=1 follows the reference's order c = C0; c = c + v*b (fused here)."""
+    rowptr = np.array([0, 3], np.int32)
+    colind = np.array([0, 1, 2], np.int32)
+    vals = np.array([1e8, 1.0, -1e8], np.float32)
+    B = np.ones((3, 1), np.float32)
+    C0 = np.array([[1.0]], np.float32)
+    got = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", accumulate=True, C0=C0)
+    # ((1 + 1e8) + 1) - 1e8 in fp32 = 0 (C0 absorbed), not 1e8 - 1e8 + 2 = 2
+    assert got[0, 0] == np.float32(np.float32(np.float32(np.float32(1) + np.float32(1e8)) + 1) - np.float32(1e8))
+
+
+def test_empty_rows_give_zero(oracle_mod):
+    rowptr = np.array([0, 0, 0], np.int32)
+    B = np.ones((3, 4), np.float32)
+    for op in ("sum", "max", "min", "mean"):
+        got = oracle_mod.spmm_f32(rowptr, np.zeros(0, np.int32), np.zeros(0, np.float32), B, op)
+        np.testing.assert_array_equal(got, np.zeros((2, 4), np.float32))
