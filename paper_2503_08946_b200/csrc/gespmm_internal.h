@@ -22,8 +22,11 @@ constexpr int kRowCost = 2;
 constexpr int kTileMaxRows = kTileWork / kRowCost;
 // Kernel geometry: one warp per work item, 8 warps per CTA.
 constexpr int kWarpsPerBlock = 8;
-// Nonzeros staged per warp refill: 32 lanes x one 128-bit colind/vals load each.
-constexpr int kChunk = 128;
+// Per-warp shared-memory stage for one item's (col, val) stream.  An item holds
+// at most kTileWork + kSeg + kRowCost - 1 nonzeros (a tile) or kSeg (a segment);
+// staging starts at the 16-byte-aligned position below the item start.
+constexpr int kStageCap = 640;
+static_assert(kTileWork + kSeg + kRowCost + 2 <= kStageCap, "stage too small for the largest item");
 // Low 40 bits of the packed plan scan carry tile work, high 24 bits segment counts.
 constexpr int kPackShift = 40;
 

@@ -9,22 +9,27 @@
 //  * One warp per work item.  An item is either a TILE of consecutive short
 //    rows (deg <= kSeg, ~kTileWork work units: nnz-balanced) or one kSeg-long
 //    SEGMENT of a long row.  Items come from the plan (gespmm_plan.cu).
-//  * Coalesced Row Caching: the warp streams the item's nonzeros in chunks of
-//    128: every lane issues ONE 128-bit load of colind and ONE of vals and
-//    writes the pairs into the warp's slice of shared memory, with col already
-//    scaled to the B-row element offset col*ldb; each pair is then read back
-//    as a broadcast (one LDS.64 per nonzero).  __syncwarp() orders the stage
-//    writes before the reads and the reads before the next refill -- the
-//    warp-scoped form of the reference's two barriers (gespmm_alg2.mir:36, :65).
-//    The next chunk is prefetched into registers while the current one is used.
+//  * Coalesced Row Caching: the warp copies the item's whole colind/vals span
+//    (<= kStageCap nonzeros) into its slice of shared memory with 16-byte
+//    cp.async per lane (fully coalesced, no register cost, one commit/wait),
+//    plus the tile's rowptr window.  One __syncwarp() publishes the stage --
+//    the warp-scoped form of the reference's staging barrier
+//    (gespmm_alg2.mir:36); another at the top of the next item orders the
+//    stage reads before the refill (the reference's second barrier, mir:65).
+//  * Persistent warps walk the work list with a warp stride; a segment runs
+//    through the same pipeline as a one-row tile (one code path: the kernel
+//    must stay inside the instruction cache).
 //  * Coarse-grained Warp Merging: each lane owns VEC consecutive columns in each
-//    of CWM column tiles, so one staged pair feeds VEC*CWM FMAs and every B-row
-//    gather is one fully coalesced 32*VEC*4-byte warp access.  U gathers are
-//    issued before the first is consumed (memory-level parallelism).
-//  * Rows inside a tile are reduced sequentially in ascending p.  A batch of U
-//    nonzeros that lies inside the current row takes the check-free fast path;
-//    a batch that crosses a row end takes the slow path, which stores finished
-//    rows (streaming stores) and steps through empty rows.
+//    of CWM column tiles, so one staged (col, val) pair feeds VEC*CWM FMAs and
+//    every B-row gather is one fully coalesced 32*VEC*4-byte warp access.
+//  * Gather pipeline: B-row gathers are issued in batches of U nonzeros into
+//    two register buffers; batch k+1 is in flight while batch k is folded, so
+//    ~2U rows per warp (4 KB at N=64) stay in flight.  The measured ceiling for
+//    this access pattern is ~19 TB/s from L2 (tools/gather_bw.cu); TMA gather4
+//    reaches only 3-7 TB/s for 256-byte rows, so the gathers stay in LDG.
+//  * Rows inside a tile are reduced sequentially in ascending p.  A batch that
+//    lies inside the current row is folded check-free; a batch that crosses a
+//    row end stores finished rows (streaming stores) and steps empty rows.
 //  * Long-row segments publish a partial; the last segment to finish (atomic
 //    ticket) combines all partials strictly in segment order and writes C, so
 //    the result is deterministic and needs no second launch.
@@ -92,17 +97,69 @@ struct Vec<4> {
   }
 };
 
-// Registers per lane: U gathers of VEC*CWM floats each in flight.
+// One B-row gather: address = base + 4*off (one IMAD.WIDE.U32) and one
+// non-coherent vector load.  `base` already includes the lane's column offset.
+template <int VEC>
+__device__ __forceinline__ void gather_off(float* d, const float* base, uint32_t off);
+template <>
+__device__ __forceinline__ void gather_off<1>(float* d, const float* base, uint32_t off) {
+  asm("{\n .reg .u64 a;\n mad.wide.u32 a, %1, 4, %2;\n ld.global.nc.f32 %0, [a];\n}"
+               : "=f"(d[0])
+               : "r"(off), "l"(base));
+}
+template <>
+__device__ __forceinline__ void gather_off<2>(float* d, const float* base, uint32_t off) {
+  asm("{\n .reg .u64 a;\n mad.wide.u32 a, %2, 4, %3;\n ld.global.nc.v2.f32 {%0, %1}, [a];\n}"
+               : "=f"(d[0]), "=f"(d[1])
+               : "r"(off), "l"(base));
+}
+template <>
+__device__ __forceinline__ void gather_off<4>(float* d, const float* base, uint32_t off) {
+  asm(
+      "{\n .reg .u64 a;\n mad.wide.u32 a, %4, 4, %5;\n ld.global.nc.v4.f32 {%0, %1, %2, %3}, [a];\n}"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(off), "l"(base));
+}
+
+// 16-byte / 4-byte global->shared async copies (LDGSTS); the 16-byte form
+// bypasses L1 for the once-read colind/vals stream.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Batch size U (a multiple of 4: the staged (col, val) pairs of a batch are
+// read with 128-bit shared loads) and buffering: two register buffers of
+// U*VEC*CWM floats, except for 8 columns per lane (one buffer, U = 4).
+#ifndef GESPMM_U_NARROW
+#define GESPMM_U_NARROW 8  // batch for <= 2 columns per lane
+#endif
+#ifndef GESPMM_DOUBLE
+#define GESPMM_DOUBLE 0  // measured: one buffer (60 regs, 32 warps/SM) beats two (spills)
+#endif
 template <int CPL>
-struct Unroll {
-  static constexpr int U = CPL >= 8 ? 2 : (CPL >= 4 ? 4 : 8);
+struct Pipe {
+  static constexpr int U = CPL >= 4 ? 4 : GESPMM_U_NARROW;
+  static constexpr bool kDouble = GESPMM_DOUBLE && CPL <= 4;
 };
 
-// Min CTAs per SM for __launch_bounds__: caps registers so >= 32 warps/SM are
-// resident (latency hiding for the dependent index->gather chain).
 #ifndef GESPMM_MINBLOCKS
 #define GESPMM_MINBLOCKS 4
 #endif
+// Min CTAs per SM for __launch_bounds__: caps registers so 32 warps/SM are
+// resident; with two buffers in flight per warp that is ~128 KB of gathers
+// per SM at N=64 (the L2 gather ceiling needs about that much).
 template <int CPL>
 struct MinBlocks {
   static constexpr int value = CPL >= 8 ? 3 : GESPMM_MINBLOCKS;
@@ -113,118 +170,47 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     spmm_kernel(const KParams P) {
   using SR = Semiring<OP>;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
-  constexpr int U = Unroll<CPL>::U;    // gathers in flight per lane
+  constexpr int U = Pipe<CPL>::U;      // gathers per batch
   constexpr int TW = 32 * VEC;         // columns per CWM tile
-  constexpr int RPV = (kTileMaxRows + 32) / 32;
-  __shared__ __align__(16) int2 stage[kWarpsPerBlock][kChunk];
+  __shared__ __align__(16) int scol[kWarpsPerBlock][kStageCap];
+  __shared__ __align__(16) float sval[kWarpsPerBlock][kStageCap];
   __shared__ int rpw[kWarpsPerBlock][kTileMaxRows + 4];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  if (t >= P.n_items) return;  // warp-uniform; the kernel uses no CTA-wide barrier
-  const int4 it = P.items[t];
   const int cb = blockIdx.y;
   const int64_t colbase = static_cast<int64_t>(cb) * (TW * CWM) + lane * VEC;
   // Lanes whose columns fall past N gather column 0 instead (always valid,
   // never stored): the gather loop carries no per-load predicate.
   bool cok[CWM];
+  const float* bw[CWM];  // B + this lane's column offset, per CWM tile
   int woff[CWM];
 #pragma unroll
   for (int w = 0; w < CWM; ++w) {
     cok[w] = colbase + w * TW < P.N;
     woff[w] = cok[w] ? static_cast<int>(colbase + w * TW) : 0;
+    bw[w] = P.B + woff[w];
   }
-  const float* __restrict__ B = P.B;
   const int64_t ldb = P.ldb;
-  int2* st = stage[warp];
+  int* const sc = scol[warp];
+  float* const sv = sval[warp];
+  int* const rp = rpw[warp];
   const bool accumulate = P.accumulate != 0;
+  const bool seed_c0 = accumulate && SR::kSeedC0;
 
   float acc[CWM][VEC];
-
-  auto bptr = [&](int x) -> const float* {
-    if (OFF32) return B + static_cast<uint32_t>(x);
-    return B + static_cast<int64_t>(x) * ldb;
-  };
-
-  // -- CRC staging: lane l covers the 4 nonzeros at cbase + 4l (128-bit loads) --
-  auto fetch = [&](int cbase, int lo, int hi, int4& c, float4& v) {
-    const int e = cbase + 4 * lane;
-    c = make_int4(0, 0, 0, 0);
-    v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e < hi && e + 4 > lo) {
-      if (P.idx_aligned && e + 4 <= P.nnz) {
-        c = __ldcs(reinterpret_cast<const int4*>(P.colind + e));
-        v = __ldcs(reinterpret_cast<const float4*>(P.vals + e));
-      } else {
-        int* cc = &c.x;
-        float* vv = &v.x;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (e + q < P.nnz && e + q >= lo && e + q < hi) {
-            cc[q] = __ldcs(P.colind + e + q);
-            vv[q] = __ldcs(P.vals + e + q);
-          }
-      }
-    }
-  };
-  auto put = [&](const int4& c, const float4& v) {
-    int4 o;
-    if (OFF32) {  // pre-scale to the B-row element offset (fits 32 bits: K*ldb < 2^32)
-      o = make_int4(static_cast<int>(static_cast<uint32_t>(c.x) * static_cast<uint32_t>(ldb)),
-                    static_cast<int>(static_cast<uint32_t>(c.y) * static_cast<uint32_t>(ldb)),
-                    static_cast<int>(static_cast<uint32_t>(c.z) * static_cast<uint32_t>(ldb)),
-                    static_cast<int>(static_cast<uint32_t>(c.w) * static_cast<uint32_t>(ldb)));
-    } else {
-      o = c;
-    }
-    int4* s = reinterpret_cast<int4*>(st + 4 * lane);
-    s[0] = make_int4(o.x, __float_as_int(v.x), o.y, __float_as_int(v.y));
-    s[1] = make_int4(o.z, __float_as_int(v.z), o.w, __float_as_int(v.w));
-  };
-
-  // Gathers for staged positions [i0, i0+U) (stage-relative), unclamped.
-  auto gather = [&](int i0, float (&vv)[U], float (&b)[U][CWM][VEC]) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int2 e = st[i0 + u];
-      vv[u] = __int_as_float(e.y);
-      const float* src = bptr(e.x);
-#pragma unroll
-      for (int w = 0; w < CWM; ++w) Vec<VEC>::ldg(b[u][w], src + woff[w]);
-    }
-  };
-  // Same, with positions clamped to ilast (no predicate on the loads).
-  auto gather_clamped = [&](int i0, int ilast, float (&vv)[U], float (&b)[U][CWM][VEC]) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int2 e = st[min(i0 + u, ilast)];
-      vv[u] = __int_as_float(e.y);
-      const float* src = bptr(e.x);
-#pragma unroll
-      for (int w = 0; w < CWM; ++w) Vec<VEC>::ldg(b[u][w], src + woff[w]);
-    }
-  };
-  auto fold = [&](float v, const float (&b)[CWM][VEC], bool first) {
+  auto set_acc = [&](float x) {
 #pragma unroll
     for (int w = 0; w < CWM; ++w)
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) acc[w][k] = SR::update(acc[w][k], v, b[w][k], first);
+      for (int k = 0; k < VEC; ++k) acc[w][k] = x;
   };
-
-  auto seed_row = [&](int64_t grow, bool seeded) {
-    if (seeded) {
-      const float* src = P.C + grow * P.ldc;
+  auto load_acc = [&](int64_t grow) {  // accumulate=1 seed: C0
+    const float* src = P.C + grow * P.ldc;
 #pragma unroll
-      for (int w = 0; w < CWM; ++w) Vec<VEC>::ld(acc[w], src + woff[w]);
-    } else {
-#pragma unroll
-      for (int w = 0; w < CWM; ++w)
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) acc[w][k] = SR::zero();
-    }
+    for (int w = 0; w < CWM; ++w) Vec<VEC>::ld(acc[w], src + woff[w]);
   };
-  auto store_row = [&](int64_t grow, int deg, const float (&r)[CWM][VEC]) {
+  auto store_row = [&](int64_t grow, int deg) {
     float* dst = P.C + grow * P.ldc;
 #pragma unroll
     for (int w = 0; w < CWM; ++w) {
@@ -234,150 +220,191 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
       if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst + woff[w]);
 #pragma unroll
       for (int k = 0; k < VEC; ++k)
-        o[k] = SR::finalize(r[w][k], deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
+        o[k] = SR::finalize(acc[w][k], deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
       Vec<VEC>::stcs(dst + woff[w], o);
     }
   };
+  auto gather = [&](float (&d)[CWM][VEC], int x) {
+#pragma unroll
+    for (int w = 0; w < CWM; ++w) {
+      if (OFF32) gather_off<VEC>(d[w], bw[w], static_cast<uint32_t>(x));
+      else Vec<VEC>::ldg(d[w], bw[w] + static_cast<int64_t>(x) * ldb);
+    }
+  };
 
-  if (it.y < 0) {
-    // ---------------- tile of consecutive short rows [r0, r1) ----------------
-    const int r0 = it.x;
-    int r1, pend;
-    if (t + 1 < P.n_items) {
-      const int4 nx = P.items[t + 1];
-      r1 = nx.x;
-      pend = nx.z;
-    } else {
-      r1 = P.M;
-      pend = P.nnz;
-    }
-    const int nr = r1 - r0;  // 1 <= nr <= kTileMaxRows (plan invariant)
-    const int pbeg = it.z;
-    int rpv[RPV];
-#pragma unroll
-    for (int i = 0; i < RPV; ++i) {
-      const int k = lane + 32 * i;
-      rpv[i] = (k <= nr) ? __ldg(P.rowptr + r0 + k) : 0;
-    }
-    int4 c;
-    float4 v;
-    fetch(pbeg & ~3, pbeg, pend, c, v);
-    int* rp = rpw[warp];
-#pragma unroll
-    for (int i = 0; i < RPV; ++i) {
-      const int k = lane + 32 * i;
-      if (k <= nr) rp[k] = rpv[i];
-    }
-    __syncwarp();
-    const bool seed = accumulate && SR::kSeedC0;
-    int row = 0;
-    int rs = pbeg;
-    int re = rp[1];
-    seed_row(r0, seed);
-    // advance past every row that ends at or before position q
-    auto advance_to = [&](int q) {
-      while (q >= re) {
-        store_row(r0 + row, re - rs, acc);
-        ++row;
-        rs = re;
-        re = rp[row + 1];
-        seed_row(r0 + row, seed);
+  // Persistent warps: warp-strided walk over the work list (no warp idles while
+  // a sibling in its CTA finishes a longer item).  Control flow is warp-uniform
+  // and the kernel uses no CTA-wide barrier.
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < P.n_items;
+       t += wstride) {
+    __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
+    const int4 it = P.items[t];
+    const bool is_tile = it.y < 0;
+    // ---- item decode: nonzero span [lo, hi) and its rows --------------------
+    // A segment is run as a one-row tile whose row ends at the segment end.
+    int lo, hi, nr, re_long = 0;
+    if (is_tile) {
+      int r1, pend;
+      if (t + 1 < P.n_items) {
+        const int4 nx = P.items[t + 1];
+        r1 = nx.x;
+        pend = nx.z;
+      } else {
+        r1 = P.M;
+        pend = P.nnz;
       }
-    };
-    if (pbeg < pend) {
-      int cbase = pbeg & ~3;
-      while (true) {
-        put(c, v);
-        __syncwarp();
-        const int nbase = cbase + kChunk;
-        const bool more = nbase < pend;
-        if (more) fetch(nbase, pbeg, pend, c, v);  // next chunk in flight during this one
-        const int q1 = min(pend, nbase);
-        for (int q = max(pbeg, cbase); q < q1; q += U) {
-          float vv[U];
-          float b[U][CWM][VEC];
-          if (q + U <= q1 && q + U <= re) {
-            // fast path: U nonzeros of the current row
-            gather(q - cbase, vv, b);
-            const bool first = SR::kFirstMsg && !accumulate && q == rs;
-#pragma unroll
-            for (int u = 0; u < U; ++u) fold(vv[u], b[u], first && u == 0);
-          } else {
-            // slow path: the batch crosses a row end or the chunk end
-            gather_clamped(q - cbase, q1 - 1 - cbase, vv, b);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              if (q + u < q1) {
-                advance_to(q + u);
-                fold(vv[u], b[u], SR::kFirstMsg && !accumulate && q + u == rs);
-              }
-            }
+      nr = r1 - it.x;  // 1 <= nr <= kTileMaxRows (plan invariant)
+      lo = it.z;
+      hi = pend;
+      for (int k = lane; k <= nr; k += 32) cp_async4(rp + k, P.rowptr + it.x + k);
+    } else {
+      nr = 1;
+      lo = it.z + it.y * kSeg;
+      re_long = __ldg(P.rowptr + it.x + 1);
+      hi = min(lo + kSeg, re_long);
+    }
+    // ---- CRC staging: colind/vals [sbase, hi) -> shared memory -------------
+    // Batches start at 4-aligned positions sbase + k*U; entries in [sbase, lo)
+    // are real neighbours (valid offsets, never folded) and the pad up to the
+    // last batch end is zeroed below (offset 0: a valid row, never folded).
+    const int sbase = lo & ~3;
+    const int send = sbase + ((hi - sbase + U - 1) / U) * U;
+    if (P.idx_aligned) {
+      for (int e = sbase + 4 * lane; e < hi; e += 128) {
+        if (e + 4 <= P.nnz) {
+          cp_async16(sc + (e - sbase), P.colind + e);
+          cp_async16(sv + (e - sbase), P.vals + e);
+        } else {
+          for (int q = e; q < P.nnz; ++q) {
+            cp_async4(sc + (q - sbase), P.colind + q);
+            cp_async4(sv + (q - sbase), P.vals + q);
           }
         }
-        __syncwarp();  // stage reads complete before the refill
-        if (!more) break;
-        cbase = nbase;
       }
-    }
-    for (;;) {  // the row in progress and any trailing empty rows
-      store_row(r0 + row, re - rs, acc);
-      if (++row >= nr) break;
-      rs = re;
-      re = rp[row + 1];
-      seed_row(r0 + row, seed);
-    }
-  } else {
-    // ---------------- one segment of a long row ------------------------------
-    const int row = it.x;
-    const int seg = it.y;
-    const int rs = it.z;
-    const int slot = it.w;
-    const int ps = rs + seg * kSeg;
-    int4 c;
-    float4 v;
-    fetch(ps & ~3, ps, ps + kSeg, c, v);  // issued before rowptr[row+1] returns
-    const int re = __ldg(P.rowptr + row + 1);
-    const int pe = min(ps + kSeg, re);
-    const int deg = re - rs;
-    const int nseg = (deg + kSeg - 1) / kSeg;
-    if (seg == 0) {
-      seed_row(row, accumulate && SR::kSeedC0);
     } else {
-#pragma unroll
-      for (int w = 0; w < CWM; ++w)
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) acc[w][k] = SR::identity();
-    }
-    const bool first0 = SR::kFirstMsg && !accumulate && seg == 0;
-    int cbase = ps & ~3;
-    while (true) {
-      put(c, v);
-      __syncwarp();
-      const int nbase = cbase + kChunk;
-      const bool more = nbase < pe;
-      if (more) fetch(nbase, ps, pe, c, v);
-      const int q1 = min(pe, nbase);
-      int q = max(ps, cbase);
-      for (; q + U <= q1; q += U) {
-        float vv[U];
-        float b[U][CWM][VEC];
-        gather(q - cbase, vv, b);
-#pragma unroll
-        for (int u = 0; u < U; ++u) fold(vv[u], b[u], first0 && u == 0 && q == ps);
+      for (int e = sbase + lane; e < hi; e += 32) {
+        cp_async4(sc + (e - sbase), P.colind + e);
+        cp_async4(sv + (e - sbase), P.vals + e);
       }
-      if (q < q1) {
-        float vv[U];
-        float b[U][CWM][VEC];
-        gather_clamped(q - cbase, q1 - 1 - cbase, vv, b);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // zero the pad [hi, send) (overwrites any neighbours cp.async brought in)
+    for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;
+    __syncwarp();
+    if (OFF32) {  // col -> B-row element offset col*ldb, once per staged entry
+      const uint32_t ldb32 = static_cast<uint32_t>(ldb);
+      for (int i = 4 * lane; i < send - sbase; i += 128) {
+        int4 c = *reinterpret_cast<int4*>(sc + i);
+        c.x = static_cast<int>(static_cast<uint32_t>(c.x) * ldb32);
+        c.y = static_cast<int>(static_cast<uint32_t>(c.y) * ldb32);
+        c.z = static_cast<int>(static_cast<uint32_t>(c.z) * ldb32);
+        c.w = static_cast<int>(static_cast<uint32_t>(c.w) * ldb32);
+        *reinterpret_cast<int4*>(sc + i) = c;
+      }
+      __syncwarp();
+    }
+
+    // ---- row state ----------------------------------------------------------
+    const int64_t grow0 = it.x;  // global row of local row 0
+    int row = 0, rs = lo, re = is_tile ? rp[1] : hi;
+    // max/min take their first message as the initial value, except when
+    // seeded (accumulate) or in a later segment (seeded with the identity).
+    const bool first_ok = SR::kFirstMsg && !accumulate && (is_tile || it.y == 0);
+    if (!is_tile && it.y > 0) set_acc(SR::identity());
+    else if (seed_c0) load_acc(grow0);
+    else set_acc(SR::zero());
+
+    // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
+    auto issue = [&](int qb, float (&b)[U][CWM][VEC]) {
+      const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
+#pragma unroll
+      for (int g = 0; g < U / 4; ++g) {
+        const int4 o = cp[g];
+        gather(b[4 * g + 0], o.x);
+        gather(b[4 * g + 1], o.y);
+        gather(b[4 * g + 2], o.z);
+        gather(b[4 * g + 3], o.w);
+      }
+    };
+    auto consume = [&](int qb, const float (&b)[U][CWM][VEC]) {
+      const float4* vp = reinterpret_cast<const float4*>(sv + (qb - sbase));
+      float v[U];
+#pragma unroll
+      for (int g = 0; g < U / 4; ++g) {
+        const float4 x = vp[g];
+        v[4 * g] = x.x, v[4 * g + 1] = x.y, v[4 * g + 2] = x.z, v[4 * g + 3] = x.w;
+      }
+      if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
+        const bool first = first_ok && qb == rs;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (q + u < q1) fold(vv[u], b[u], first0 && q + u == ps);
+#pragma unroll
+          for (int w = 0; w < CWM; ++w)
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+              acc[w][k] = SR::update(acc[w][k], v[u], b[u][w][k], first && u == 0);
+        return;
       }
-      __syncwarp();
-      if (!more) break;
-      cbase = nbase;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // slow path: element by element
+        const int p = qb + u;
+        if (p < lo || p >= hi) continue;
+        while (p >= re) {  // rows ending at or before p are complete (tiles only)
+          store_row(grow0 + row, re - rs);
+          ++row;
+          rs = re;
+          re = rp[row + 1];
+          if (seed_c0) load_acc(grow0 + row);
+          else set_acc(SR::zero());
+        }
+        const bool first = first_ok && p == rs;
+#pragma unroll
+        for (int w = 0; w < CWM; ++w)
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) acc[w][k] = SR::update(acc[w][k], v[u], b[u][w][k], first);
+      }
+    };
+    if (lo < hi) {
+      if (Pipe<CPL>::kDouble) {
+        float ba[U][CWM][VEC];
+        float bb[U][CWM][VEC];
+        issue(sbase, ba);
+        for (int qb = sbase;; qb += 2 * U) {
+          if (qb + U < hi) issue(qb + U, bb);
+          consume(qb, ba);
+          if (qb + U >= hi) break;
+          if (qb + 2 * U < hi) issue(qb + 2 * U, ba);
+          consume(qb + U, bb);
+          if (qb + 2 * U >= hi) break;
+        }
+      } else {
+        float ba[U][CWM][VEC];
+        for (int qb = sbase; qb < hi; qb += U) {
+          issue(qb, ba);
+          consume(qb, ba);
+        }
+      }
     }
-    // publish this segment's partial, then take a ticket
+
+    if (is_tile) {
+      // ---- the row in progress and any trailing empty rows -------------------
+      for (;;) {
+        store_row(grow0 + row, re - rs);
+        if (++row >= nr) break;
+        rs = re;
+        re = rp[row + 1];
+        if (seed_c0) load_acc(grow0 + row);
+        else set_acc(SR::zero());
+      }
+      continue;
+    }
+    // ---- long-row segment: publish the partial, then take a ticket -----------
+    const int seg = it.y;
+    const int slot = it.w;
+    const int deg = re_long - it.z;
+    const int nseg = (deg + kSeg - 1) / kSeg;
     float* part = P.partials + static_cast<int64_t>(slot + seg) * P.ldp;
 #pragma unroll
     for (int w = 0; w < CWM; ++w)
@@ -388,41 +415,53 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     int* counter = P.counters + static_cast<int64_t>(slot) * P.ncb + cb;
     if (lane == 0) ticket = atomicAdd(counter, 1);
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    if (ticket == nseg - 1) {
-      // last segment: combine all partials strictly left to right
-      __threadfence();
-      const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp;
-      float r[CWM][VEC];
+    if (ticket != nseg - 1) continue;
+    // last segment: combine all partials strictly left to right
+    __threadfence();
+    const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp;
 #pragma unroll
-      for (int w = 0; w < CWM; ++w) Vec<VEC>::ldcg(r[w], base + woff[w]);
-      constexpr int CU = 4;
-      for (int s = 1; s < nseg; s += CU) {
-        float pv[CU][CWM][VEC];
+    for (int w = 0; w < CWM; ++w) Vec<VEC>::ldcg(acc[w], base + woff[w]);
+    constexpr int CU = 4;
+    for (int s = 1; s < nseg; s += CU) {
+      float pv[CU][CWM][VEC];
 #pragma unroll
-        for (int u = 0; u < CU; ++u) {
-          const int ss = min(s + u, nseg - 1);
+      for (int u = 0; u < CU; ++u) {
+        const int ss = min(s + u, nseg - 1);
+#pragma unroll
+        for (int w = 0; w < CWM; ++w)
+          Vec<VEC>::ldcg(pv[u][w], base + static_cast<int64_t>(ss) * P.ldp + woff[w]);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u)
+        if (s + u < nseg)
 #pragma unroll
           for (int w = 0; w < CWM; ++w)
-            Vec<VEC>::ldcg(pv[u][w], base + static_cast<int64_t>(ss) * P.ldp + woff[w]);
-        }
 #pragma unroll
-        for (int u = 0; u < CU; ++u)
-          if (s + u < nseg)
-#pragma unroll
-            for (int w = 0; w < CWM; ++w)
-#pragma unroll
-              for (int k = 0; k < VEC; ++k) r[w][k] = SR::combine(r[w][k], pv[u][w][k]);
-      }
-      store_row(row, deg, r);
-      if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
+            for (int k = 0; k < VEC; ++k) acc[w][k] = SR::combine(acc[w][k], pv[u][w][k]);
     }
-  }
+    store_row(grow0, deg);
+    if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
+  }  // item loop
 }
 
 template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32>
 cudaError_t launch_t(const KParams& p, cudaStream_t s) {
-  const int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks == 0) return cudaSuccess;
+  // persistent grid: every resident CTA slot once (per column block)
+  static thread_local int cached_dev = -1, cached_slots = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32>,
+                                                  kWarpsPerBlock * 32, 0);
+    cached_slots = sms * (per_sm > 0 ? per_sm : 1);
+    cached_dev = dev;
+  }
+  const int64_t slots = (cached_slots + p.ncb - 1) / p.ncb;
+  if (blocks > slots) blocks = slots;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(p.ncb), 1);
   spmm_kernel<OP, VEC, CWM, OFF32><<<grid, kWarpsPerBlock * 32, 0, s>>>(p);
   return cudaGetLastError();
