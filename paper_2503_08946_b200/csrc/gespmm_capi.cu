@@ -94,6 +94,53 @@ gespmm_status_t ensure_workspace(gespmm_plan_s* plan, int64_t ldp, int ncb, cuda
   return GESPMM_OK;
 }
 
+std::mutex& host_ws_mutex() {
+  static std::mutex m;
+  return m;
+}
+
+// Side stream + event for the host entry point's copies, one per device.
+gespmm_status_t side_stream(cudaStream_t* s, cudaEvent_t* ev) {
+  struct Side {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev = nullptr;
+  };
+  static Side side[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Side& x = side[dev & 63];
+  if (!x.s) {
+    cudaError_t e = cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "side stream");
+  }
+  *s = x.s;
+  *ev = x.ev;
+  return GESPMM_OK;
+}
+
+// Grow-only device workspace for the host entry point, one per device.
+gespmm_status_t host_workspace(int64_t bytes, char** out) {
+  struct Ws {
+    char* p = nullptr;
+    int64_t cap = 0;
+  };
+  static Ws ws[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Ws& w = ws[dev & 63];
+  if (bytes > w.cap) {
+    if (w.p) cudaFree(w.p);
+    w.p = nullptr;
+    w.cap = 0;
+    cudaError_t e = cudaMalloc(&w.p, static_cast<size_t>(bytes > 0 ? bytes : 256));
+    if (e != cudaSuccess) return cuda_fail(e, "host-path workspace");
+    w.cap = bytes;
+  }
+  *out = w.p;
+  return GESPMM_OK;
+}
+
 }  // namespace
 }  // namespace gespmm
 
@@ -273,61 +320,76 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
   if (st != GESPMM_OK) return st;
   cudaStream_t s = as_stream(stream);
-  // device copies: B and C packed with ld = N
-  int32_t* d_rp = nullptr;
-  int32_t* d_ci = nullptr;
-  float* d_v = nullptr;
-  float* d_B = nullptr;
-  float* d_C = nullptr;
-  auto cleanup = [&]() {
-    cudaFreeAsync(d_rp, s);
-    cudaFreeAsync(d_ci, s);
-    cudaFreeAsync(d_v, s);
-    cudaFreeAsync(d_B, s);
-    cudaFreeAsync(d_C, s);
-    cudaStreamSynchronize(s);
-  };
+  // Device staging: one grow-only workspace per device, reused across calls
+  // (a fresh 0.7 GB allocation per call costs more than the kernel).
+  std::lock_guard<std::mutex> lock(host_ws_mutex());
+  auto al = [](int64_t bytes) { return (bytes + 255) & ~int64_t(255); };
+  const int64_t b_rp = al((M + 1) * 4), b_ci = al(nnz * 4), b_v = al(nnz * 4),
+                b_B = al(K * N * 4), b_C = al(M * N * 4);
+  char* ws = nullptr;
+  st = host_workspace(b_rp + b_ci + b_v + b_B + b_C, &ws);
+  if (st != GESPMM_OK) return st;
+  auto* d_rp = reinterpret_cast<int32_t*>(ws);
+  auto* d_ci = reinterpret_cast<int32_t*>(ws + b_rp);
+  auto* d_v = reinterpret_cast<float*>(ws + b_rp + b_ci);
+  auto* d_B = reinterpret_cast<float*>(ws + b_rp + b_ci + b_v);
+  auto* d_C = reinterpret_cast<float*>(ws + b_rp + b_ci + b_v + b_B);
   cudaError_t e = cudaSuccess;
-  auto al = [&](auto** p, size_t n) {
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(p), n > 0 ? n : 16, s);
-  };
-  al(&d_rp, static_cast<size_t>(M + 1) * 4);
-  al(&d_ci, static_cast<size_t>(nnz) * 4);
-  al(&d_v, static_cast<size_t>(nnz) * 4);
-  al(&d_B, static_cast<size_t>(K * N) * 4);
-  al(&d_C, static_cast<size_t>(M * N) * 4);
-  if (e != cudaSuccess) {
-    cleanup();
-    return cuda_fail(e, "device allocation");
-  }
   auto h2d = [&](void* d, const void* h, size_t n) {
     if (e == cudaSuccess && n) e = cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s);
   };
+  // The structure goes first on `s`; vals, B (and C0) go on a side stream so
+  // the plan build (which synchronizes `s`) overlaps their transfer.
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev = nullptr;
+  st = side_stream(&s2, &ev);
+  if (st != GESPMM_OK) return st;
+  cudaEvent_t ev0 = nullptr;
+  e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev0, s);  // s2 must not overtake prior work on s
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, ev0, 0);
+  if (ev0) cudaEventDestroy(ev0);
   h2d(d_rp, rowptr, static_cast<size_t>(M + 1) * 4);
   h2d(d_ci, colind, static_cast<size_t>(nnz) * 4);
-  h2d(d_v, vals, static_cast<size_t>(nnz) * 4);
-  if (e == cudaSuccess && K * N > 0)
-    e = cudaMemcpy2DAsync(d_B, N * 4, B, ldb * 4, N * 4, K, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && accumulate && M * N > 0)
-    e = cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s);
+  auto h2d2 = [&](void* d, const void* h, size_t n) {
+    if (e == cudaSuccess && n) e = cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s2);
+  };
+  h2d2(d_v, vals, static_cast<size_t>(nnz) * 4);
+  if (e == cudaSuccess && K * N > 0) {
+    if (ldb == N) h2d2(d_B, B, static_cast<size_t>(K * N) * 4);
+    else e = cudaMemcpy2DAsync(d_B, N * 4, B, ldb * 4, N * 4, K, cudaMemcpyHostToDevice, s2);
+  }
+  if (e == cudaSuccess && accumulate && M * N > 0) {
+    if (ldc == N) h2d2(d_C, C, static_cast<size_t>(M * N) * 4);
+    else e = cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s2);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(ev, s2);
   if (e != cudaSuccess) {
-    cleanup();
+    cudaStreamSynchronize(s2);
     return cuda_fail(e, "host to device copy");
   }
   gespmm_plan_t plan = nullptr;
   st = gespmm_plan_create(&plan, M, K, nnz, d_rp, d_ci, 1, stream);
-  if (st == GESPMM_OK)
-    st = gespmm_plan_execute(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate, stream);
-  if (st == GESPMM_OK && M * N > 0) {
-    e = cudaMemcpy2DAsync(C, ldc * 4, d_C, N * 4, N * 4, M, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) st = cuda_fail(e, "device to host copy");
+  if (st != GESPMM_OK) {
+    cudaStreamSynchronize(s2);
+    return st;
   }
-  if (plan) {
-    cudaStreamSynchronize(s);
+  e = cudaStreamWaitEvent(s, ev, 0);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(s2);
     gespmm_plan_destroy(plan);
+    return cuda_fail(e, "stream join");
   }
-  cleanup();
+  st = gespmm_plan_execute(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate, stream);
+  if (st == GESPMM_OK && M * N > 0) {
+    if (ldc == N)
+      e = cudaMemcpyAsync(C, d_C, static_cast<size_t>(M * N) * 4, cudaMemcpyDeviceToHost, s);
+    else
+      e = cudaMemcpy2DAsync(C, ldc * 4, d_C, N * 4, N * 4, M, cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (st == GESPMM_OK && e != cudaSuccess) st = cuda_fail(e, "device to host copy");
+  gespmm_plan_destroy(plan);
   return st;
 }
 

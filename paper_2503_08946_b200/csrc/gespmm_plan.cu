@@ -144,8 +144,25 @@ gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K
   return GESPMM_OK;
 }
 
+// Plan temporaries are stream-ordered allocations from the device's default
+// memory pool; keep that pool's memory mapped across synchronizations
+// (release threshold 0 would unmap and remap ~25 MB per plan build).
+static void keep_pool_resident() {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev & 63]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  done[dev & 63] = true;
+}
+
 gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* colind,
                            bool check_colind, cudaStream_t s) {
+  keep_pool_resident();
   const int64_t M = plan->M;
   const int M32 = static_cast<int>(M);
   const int nnz32 = static_cast<int>(plan->nnz);

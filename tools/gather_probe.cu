@@ -1,0 +1,67 @@
+// gather_probe.cu -- the gather-only ceiling for a given column stream.
+//
+// Replays idx[] (e.g. a CSR's colind) as 256-byte B-row gathers (N = 64 fp32)
+// in the SpMM's order: each warp walks contiguous spans of `span` positions in
+// batches of U loads in flight, warps grid-stride over spans.  Nothing else is
+// read or written (no colind staging, no C), so the time is a lower bound for
+// any kernel that gathers the same rows in the same order.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC
+//          -o tools/libgather_probe.so tools/gather_probe.cu
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+template <int U>
+__global__ void __launch_bounds__(256) probe(const float* __restrict__ B, const int* __restrict__ idx,
+                                             int64_t nidx, int span, float* sink) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    for (int64_t base = s0; base < s1; base += U) {
+      const int my = (lane < U && base + lane < s1) ? __ldg(idx + base + lane) : 0;
+      float2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = __shfl_sync(0xffffffffu, my, u);
+        v[u] = __ldg(reinterpret_cast<const float2*>(B + static_cast<int64_t>(r) * 64) + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a0 += v[u].x;
+        a1 += v[u].y;
+      }
+    }
+  }
+  if (a0 == 1234.5f) sink[0] = a1;
+}
+
+extern "C" float gather_probe(const float* B, const int* idx, int64_t nidx, int U, int span,
+                              int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 2; ++r) {
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    const int grid = sms * blocks_per_sm;
+    if (U == 8) probe<8><<<grid, 256>>>(B, idx, nidx, span, sink);
+    else if (U == 16) probe<16><<<grid, 256>>>(B, idx, nidx, span, sink);
+    else probe<4><<<grid, 256>>>(B, idx, nidx, span, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 2 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaGetLastError() == cudaSuccess ? best : -1.f;
+}

@@ -1,0 +1,42 @@
+"""Gather ceiling for the config-2 matrix: replays its colind stream through
+tools/libgather_probe.so (pure B-row gathers, N=64, L2 flushed before each
+rep) at several loads-in-flight / occupancy points.  Prints one JSON line."""
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2503_08946_b200 import workloads as W  # noqa: E402
+
+
+def main():
+    L = ctypes.CDLL(os.path.join(ROOT, "tools", "libgather_probe.so"))
+    L.gather_probe.restype = ctypes.c_float
+    L.gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_int64]
+    dev = torch.device("cuda:0")
+    csr = W.rmat_csr(20, 16 * 2**20, seed=3, device=dev)
+    B = W.dense_torch(csr.K, 64, seed=2, device=dev)
+    sink = torch.zeros(4, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    nnz = csr.nnz
+    out = {"nnz": nnz, "gather_bytes": nnz * 256, "results": []}
+    streams = {"csr_order": csr.colind,
+               "shuffled": csr.colind[torch.randperm(nnz, device=dev)].contiguous()}
+    for name, idx in streams.items():
+        for U, bps in ((8, 8), (16, 8), (8, 4), (16, 4)):
+            ms = L.gather_probe(B.data_ptr(), idx.data_ptr(), nnz, U, 256, bps, 5, sink.data_ptr(),
+                                flush.data_ptr(), flush.numel())
+            out["results"].append({"stream": name, "U": U, "warps_per_sm": 8 * bps, "ms": ms,
+                                   "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
