@@ -326,3 +326,28 @@ def test_config2_full_size_bit_exact(cuda, oracle_mod, op):
     want = oracle_mod.spmm_f32(csr.rowptr.cpu().numpy(), csr.colind.cpu().numpy(),
                                csr.vals.cpu().numpy(), B.cpu().numpy(), op, seg_len=SEG)
     np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def test_reference_side_cpp_adapter(cuda, tmp_path):
+    """The C++ binding a raceset maintainer adds (examples/raceset_adapter.cpp,
+    linked against the reference's own library) computes the shipped instance
+    through libgespmm.so; matches the reference interpreter's full-launch C."""
+    import os
+    import subprocess
+
+    from test_instance import golden_inst_text
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples",
+                       "raceset_adapter")
+    if not os.path.exists(exe):
+        pytest.skip("examples/raceset_adapter not built (reference tree absent at build time)")
+    for name in ("ref_gespmm_small_full.json", "rnd_ragged_c0.json"):
+        g = load_golden(name)
+        inst = tmp_path / (name + ".inst")
+        inst.write_text(golden_inst_text(g, "adapter"))
+        out = subprocess.run([exe, str(inst)], capture_output=True, text=True, timeout=120)
+        assert out.returncode == 0, out.stderr
+        got = np.array([float(x) for x in out.stdout.split()], np.float64)
+        ref = np.asarray(g["C"], np.float64)
+        scale = np.maximum(np.abs(ref), 1.0)
+        assert np.all(np.abs(got - ref) <= 1e-5 * scale * 64), np.abs(got - ref).max()
