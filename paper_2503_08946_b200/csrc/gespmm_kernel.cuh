@@ -184,6 +184,15 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #ifndef GESPMM_U_NARROW
 #define GESPMM_U_NARROW 8  // batch for <= 2 columns per lane
 #endif
+#ifndef GESPMM_ABL_NOSTORE
+#define GESPMM_ABL_NOSTORE 0
+#endif
+#ifndef GESPMM_ABL_NOGATHER
+#define GESPMM_ABL_NOGATHER 0
+#endif
+#ifndef GESPMM_FRAG_SLOW
+#define GESPMM_FRAG_SLOW 0
+#endif
 #ifndef GESPMM_DOUBLE
 #define GESPMM_DOUBLE 0  // measured: one buffer (60 regs, 32 warps/SM) beats two (spills)
 #endif
@@ -244,27 +253,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
 #pragma unroll
       for (int k = 0; k < VEC; ++k) acc[w][k] = x;
   };
-  auto load_acc = [&](int64_t grow) {  // accumulate=1 seed: C0
-    const float* src = P.C + grow * P.ldc;
+  // C rows are addressed through a running pointer (crow = C + row*ldc + the
+  // lane's column), advanced by ldc per row: no 64-bit multiply per row.
+  auto load_acc = [&](const float* src) {  // accumulate=1 seed: C0
 #pragma unroll
-    for (int w = 0; w < CWM; ++w) Vec<VEC>::ld(acc[w], src + woff[w]);
+    for (int w = 0; w < CWM; ++w) Vec<VEC>::ld(acc[w], src + (woff[w] - woff[0]));
   };
-  auto store_row = [&](int64_t grow, int deg) {
-    float* dst = P.C + grow * P.ldc;
+  auto store_row = [&](float* dst, int deg) {
+    if (GESPMM_ABL_NOSTORE) return;  // ablation builds only
 #pragma unroll
     for (int w = 0; w < CWM; ++w) {
       if (!cok[w]) continue;
       float o[VEC];
       float c0[VEC];
-      if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst + woff[w]);
+      if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst + (woff[w] - woff[0]));
 #pragma unroll
       for (int k = 0; k < VEC; ++k)
         o[k] = SR::finalize(acc[w][k], deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
-      Vec<VEC>::stcs(dst + woff[w], o);
+      Vec<VEC>::stcs(dst + (woff[w] - woff[0]), o);
     }
   };
   const uint64_t bpol = GESPMM_BHINT ? policy_evict_last() : 0;
   auto gather = [&](float (&d)[CWM][VEC], int x) {
+    if (GESPMM_ABL_NOGATHER) {  // ablation builds only
+#pragma unroll
+      for (int w = 0; w < CWM; ++w)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) d[w][k] = __int_as_float(x + k);
+      return;
+    }
 #pragma unroll
     for (int w = 0; w < CWM; ++w) {
       if (OFF32) gather_off<VEC>(d[w], bw[w], static_cast<uint32_t>(x), bpol);
@@ -348,12 +365,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
 
     // ---- row state ----------------------------------------------------------
     const int64_t grow0 = it.x;  // global row of local row 0
+    const int64_t ldc = P.ldc;
+    float* crow = P.C + grow0 * ldc + woff[0];
     int row = 0, rs = lo, re = is_tile ? rp[1] : hi;
     // max/min take their first message as the initial value, except when
     // seeded (accumulate) or in a later segment (seeded with the identity).
     const bool first_ok = SR::kFirstMsg && !accumulate && (is_tile || it.y == 0);
     if (!is_tile && it.y > 0) set_acc(SR::identity());
-    else if (seed_c0) load_acc(grow0);
+    else if (seed_c0) load_acc(crow);
     else set_acc(SR::zero());
 
     // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
@@ -387,16 +406,49 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
               acc[w][k] = SR::update(acc[w][k], v[u], b[u][w][k], first && u == 0);
         return;
       }
+#if GESPMM_FRAG_SLOW
+      // slow path: fold the batch row fragment by row fragment (one predicated
+      // fold block and one row-advance block, whatever U is)
+      const int qe = min(qb + U, hi);
+      int qq = max(qb, lo);
+      for (;;) {
+        const int lim = min(qe, re);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = qb + u;
+          const bool on = p >= qq && p < lim;
+          const bool first = first_ok && p == rs;
+#pragma unroll
+          for (int w = 0; w < CWM; ++w)
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+              const float nv = SR::update(acc[w][k], v[u], b[u][w][k], first);
+              acc[w][k] = on ? nv : acc[w][k];
+            }
+        }
+        qq = lim;
+        if (qq >= qe) break;
+        // qq == re: the current row is complete (tiles only)
+        store_row(crow, re - rs);
+        ++row;
+        crow += ldc;
+        rs = re;
+        re = rp[row + 1];
+        if (seed_c0) load_acc(crow);
+        else set_acc(SR::zero());
+      }
+#else
 #pragma unroll
       for (int u = 0; u < U; ++u) {  // slow path: element by element
         const int p = qb + u;
         if (p < lo || p >= hi) continue;
         while (p >= re) {  // rows ending at or before p are complete (tiles only)
-          store_row(grow0 + row, re - rs);
+          store_row(crow, re - rs);
           ++row;
+          crow += ldc;
           rs = re;
           re = rp[row + 1];
-          if (seed_c0) load_acc(grow0 + row);
+          if (seed_c0) load_acc(crow);
           else set_acc(SR::zero());
         }
         const bool first = first_ok && p == rs;
@@ -405,6 +457,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
 #pragma unroll
           for (int k = 0; k < VEC; ++k) acc[w][k] = SR::update(acc[w][k], v[u], b[u][w][k], first);
       }
+#endif
     };
     if (lo < hi) {
       if (Pipe<CPL>::kDouble) {
@@ -442,11 +495,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     if (is_tile) {
       // ---- the row in progress and any trailing empty rows -------------------
       for (;;) {
-        store_row(grow0 + row, re - rs);
+        store_row(crow, re - rs);
         if (++row >= nr) break;
+        crow += ldc;
         rs = re;
         re = rp[row + 1];
-        if (seed_c0) load_acc(grow0 + row);
+        if (seed_c0) load_acc(crow);
         else set_acc(SR::zero());
       }
       continue;
@@ -490,7 +544,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
 #pragma unroll
             for (int k = 0; k < VEC; ++k) acc[w][k] = SR::combine(acc[w][k], pv[u][w][k]);
     }
-    store_row(grow0, deg);
+    store_row(crow, deg);
     if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
   }  // item loop
 }
