@@ -52,6 +52,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--soak-s", type=float, default=1.5)
+    ap.add_argument("--variant", default="", help="kernel variant override (testing), e.g. vec1_lpr32_cwm2")
     ap.add_argument("--ref-sample-products", type=int, default=800_000,
                     help="--impl reference: nnz*N products per step (bounds interpreter RAM)")
     return ap.parse_args()
@@ -262,7 +263,8 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2503_08946_b200.spmm import Plan, csr_spmm_host, partition_rows
+    from paper_2503_08946_b200.spmm import (Plan, csr_spmm_host, partition_rows, set_variant_override,
+                                            variant_name)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -276,6 +278,8 @@ def main():
 
     spec = workload_spec(args.workload)
     N = spec["N"]
+    if args.variant:
+        set_variant_override(args.variant)
     csr, B = make_workload(spec, dev)
     M_all, K, nnz_all = csr.M, csr.K, csr.nnz
     stream = torch.cuda.current_stream(dev)
@@ -425,6 +429,7 @@ def main():
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]),
+            "kernel_variant": variant_name(N, B, C),
             "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
         }
         print(json.dumps(line))

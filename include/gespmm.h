@@ -51,7 +51,9 @@ extern "C" {
 #define GESPMM_VERSION_MAJOR 0
 #define GESPMM_VERSION_MINOR 1
 /* Long-row segment length (nonzeros).  Part of the numerical contract. */
+#ifndef GESPMM_SEGMENT_LEN
 #define GESPMM_SEGMENT_LEN 256
+#endif
 
 /* Status codes.  Mirrors the reference's ErrorKind values that can arise on
  * this path (reference include/raceset/error.hpp:10-32):

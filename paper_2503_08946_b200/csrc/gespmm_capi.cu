@@ -6,7 +6,9 @@
 // Reference errors are C++ exceptions raceset::Error{ErrorKind}
 // (include/raceset/error.hpp:36-56); here they are status codes plus a
 // thread-local detail string with the same wording.
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -25,6 +27,27 @@ std::string g_variant_override;  // test hook; "" = heuristic
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+Trace::Trace(const char* s) : scope(s) {
+  const char* e = std::getenv("GESPMM_TRACE");
+  on = e && *e && *e != '0';
+  if (on) t0 = last = now_ms();
+}
+
+void Trace::mark(const char* phase, cudaStream_t stream) {
+  if (!on) return;
+  cudaStreamSynchronize(stream);
+  const double t = now_ms();
+  std::fprintf(stderr, "[gespmm trace] %s %-24s %8.3f ms (total %8.3f)\n", scope, phase, t - last,
+               t - t0);
+  last = t;
+}
 
 gespmm_status_t fail(gespmm_status_t s, const std::string& msg) {
   g_last_error = msg;
@@ -323,12 +346,14 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   // Device staging: one grow-only workspace per device, reused across calls
   // (a fresh 0.7 GB allocation per call costs more than the kernel).
   std::lock_guard<std::mutex> lock(host_ws_mutex());
+  Trace tr("host");
   auto al = [](int64_t bytes) { return (bytes + 255) & ~int64_t(255); };
   const int64_t b_rp = al((M + 1) * 4), b_ci = al(nnz * 4), b_v = al(nnz * 4),
                 b_B = al(K * N * 4), b_C = al(M * N * 4);
   char* ws = nullptr;
   st = host_workspace(b_rp + b_ci + b_v + b_B + b_C, &ws);
   if (st != GESPMM_OK) return st;
+  tr.mark("workspace", s);
   auto* d_rp = reinterpret_cast<int32_t*>(ws);
   auto* d_ci = reinterpret_cast<int32_t*>(ws + b_rp);
   auto* d_v = reinterpret_cast<float*>(ws + b_rp + b_ci);
@@ -344,6 +369,7 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   cudaEvent_t ev = nullptr;
   st = side_stream(&s2, &ev);
   if (st != GESPMM_OK) return st;
+  if (std::getenv("GESPMM_NO_SIDE_STREAM")) s2 = s;  // debug switch
   cudaEvent_t ev0 = nullptr;
   e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(ev0, s);  // s2 must not overtake prior work on s
@@ -374,13 +400,16 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
     cudaStreamSynchronize(s2);
     return st;
   }
+  tr.mark("structure H2D + plan", s);
   e = cudaStreamWaitEvent(s, ev, 0);
   if (e != cudaSuccess) {
     cudaStreamSynchronize(s2);
     gespmm_plan_destroy(plan);
     return cuda_fail(e, "stream join");
   }
+  tr.mark("values/B H2D (joined)", s);
   st = gespmm_plan_execute(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate, stream);
+  tr.mark("kernel", s);
   if (st == GESPMM_OK && M * N > 0) {
     if (ldc == N)
       e = cudaMemcpyAsync(C, d_C, static_cast<size_t>(M * N) * 4, cudaMemcpyDeviceToHost, s);
@@ -388,8 +417,10 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
       e = cudaMemcpy2DAsync(C, ldc * 4, d_C, N * 4, N * 4, M, cudaMemcpyDeviceToHost, s);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  tr.mark("C D2H", s);
   if (st == GESPMM_OK && e != cudaSuccess) st = cuda_fail(e, "device to host copy");
   gespmm_plan_destroy(plan);
+  tr.mark("plan destroy", s);
   return st;
 }
 

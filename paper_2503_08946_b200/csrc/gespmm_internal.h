@@ -59,6 +59,16 @@ struct KParams {
   int off32;               // K*ldb <= 2^32: stage 32-bit B-row element offsets
 };
 
+// GESPMM_TRACE=1: phase timings of the host entry point and the plan build on
+// stderr (each phase is synchronized; diagnostics only).
+struct Trace {
+  bool on = false;
+  double t0 = 0, last = 0;
+  const char* scope = "";
+  explicit Trace(const char* s);
+  void mark(const char* phase, cudaStream_t stream);
+};
+
 void set_error(const std::string& msg);
 gespmm_status_t fail(gespmm_status_t s, const std::string& msg);
 gespmm_status_t cuda_fail(cudaError_t e, const char* what);

@@ -289,6 +289,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     }
   };
 
+  // acc += v * b per the semiring; sum/mean column pairs go through FFMA2
+  // (Blackwell's packed fp32 FMA: two independent RN FMAs, bit-identical)
+  auto fold = [&](float v, const float (&bb)[CWM][VEC], bool first) {
+#pragma unroll
+    for (int w = 0; w < CWM; ++w) {
+      if (SR::kFma2 && VEC >= 2) {
+#pragma unroll
+        for (int k = 0; k < VEC; k += 2) fma2_rn(acc[w][k], acc[w][k + 1], v, bb[w][k], bb[w][k + 1]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[w][k] = SR::update(acc[w][k], v, bb[w][k], first);
+      }
+    }
+  };
+
   // Persistent warps: warp-strided walk over the work list (no warp idles while
   // a sibling in its CTA finishes a longer item).  Control flow is warp-uniform
   // and the kernel uses no CTA-wide barrier.
@@ -398,12 +413,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
         const bool first = first_ok && qb == rs;
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int w = 0; w < CWM; ++w)
-#pragma unroll
-            for (int k = 0; k < VEC; ++k)
-              acc[w][k] = SR::update(acc[w][k], v[u], b[u][w][k], first && u == 0);
+        for (int u = 0; u < U; ++u) fold(v[u], b[u], first && u == 0);
         return;
       }
 #if GESPMM_FRAG_SLOW
@@ -451,11 +461,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
           if (seed_c0) load_acc(crow);
           else set_acc(SR::zero());
         }
-        const bool first = first_ok && p == rs;
-#pragma unroll
-        for (int w = 0; w < CWM; ++w)
-#pragma unroll
-          for (int k = 0; k < VEC; ++k) acc[w][k] = SR::update(acc[w][k], v[u], b[u][w][k], first);
+        fold(v[u], b[u], first_ok && p == rs);
       }
 #endif
     };

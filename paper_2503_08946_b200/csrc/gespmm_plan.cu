@@ -22,6 +22,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "gespmm_internal.h"
 
@@ -149,6 +150,7 @@ gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K
 // (release threshold 0 would unmap and remap ~25 MB per plan build).
 static void keep_pool_resident() {
   static bool done[64] = {};
+  if (std::getenv("GESPMM_NO_POOL_RESIDENT")) return;  // debug switch
   int dev = 0;
   cudaGetDevice(&dev);
   if (done[dev & 63]) return;
@@ -201,6 +203,8 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
     tmp = take(tmp_bytes);
     (void)bytes;
   }
+  Trace tr("plan");
+  tr.mark("alloc temporaries", s);
   const unsigned blocks = static_cast<unsigned>((M + 255) / 256);
   cudaMemsetAsync(err, 0, 2 * sizeof(int), s);
   k_rows<<<blocks, 256, 0, s>>>(rowptr, M32, nnz32, packed, err);
@@ -219,6 +223,7 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
   tb = tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pos, M32, s);
   k_totals<<<1, 1, 0, s>>>(packed, E, cnt, pos, M32, err, tot);
+  tr.mark("rows/validate/scan/count", s);
   Totals h{};
   cudaMemcpyAsync(&h, tot, sizeof(Totals), cudaMemcpyDeviceToHost, s);
   ce = cudaStreamSynchronize(s);
@@ -239,9 +244,11 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
     cudaFreeAsync(arena, s);
     return cuda_fail(ce, "plan items");
   }
+  tr.mark("totals D2H + items alloc", s);
   k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, plan->items);
   ce = cudaGetLastError();
   cudaFreeAsync(arena, s);
+  tr.mark("emit", s);
   if (ce != cudaSuccess) return cuda_fail(ce, "plan emit");
   return GESPMM_OK;
 }

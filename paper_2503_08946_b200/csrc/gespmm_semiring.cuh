@@ -20,9 +20,22 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cstdint>
+
 #include "gespmm.h"
 
 namespace gespmm {
+
+// Blackwell packed fp32 FMA (FFMA2): two independent round-to-nearest FMAs
+// a_i = fma(v, b_i, a_i) in one instruction -- bit-identical to two __fmaf_rn.
+__device__ __forceinline__ void fma2_rn(float& a0, float& a1, float v, float b0, float b1) {
+  uint64_t acc, bb, vv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(vv) : "f"(v));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(vv), "l"(bb));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+}
 
 template <gespmm_reduce_t OP>
 struct Semiring;
@@ -31,6 +44,7 @@ template <>
 struct Semiring<GESPMM_REDUCE_SUM> {
   static constexpr bool kSeedC0 = true;   // accumulate: the chain starts at C0
   static constexpr bool kFirstMsg = false;
+  static constexpr bool kFma2 = true;     // update() is a plain FMA: pairs -> FFMA2
   __device__ __forceinline__ static float zero() { return 0.0f; }
   __device__ __forceinline__ static float identity() { return 0.0f; }
   __device__ __forceinline__ static float update(float acc, float v, float b, bool) {
@@ -46,6 +60,7 @@ template <>
 struct Semiring<GESPMM_REDUCE_MEAN> {
   static constexpr bool kSeedC0 = false;  // C0 is added after the division
   static constexpr bool kFirstMsg = false;
+  static constexpr bool kFma2 = true;
   __device__ __forceinline__ static float zero() { return 0.0f; }
   __device__ __forceinline__ static float identity() { return 0.0f; }
   __device__ __forceinline__ static float update(float acc, float v, float b, bool) {
@@ -64,6 +79,7 @@ template <>
 struct Semiring<GESPMM_REDUCE_MAX> {
   static constexpr bool kSeedC0 = true;
   static constexpr bool kFirstMsg = true;  // acc starts at the first message
+  static constexpr bool kFma2 = false;
   __device__ __forceinline__ static float zero() { return 0.0f; }
   __device__ __forceinline__ static float identity() { return -CUDART_INF_F; }
   __device__ __forceinline__ static float better(float m, float acc) { return (m > acc) ? m : acc; }
@@ -83,6 +99,7 @@ template <>
 struct Semiring<GESPMM_REDUCE_MIN> {
   static constexpr bool kSeedC0 = true;
   static constexpr bool kFirstMsg = true;
+  static constexpr bool kFma2 = false;
   __device__ __forceinline__ static float zero() { return 0.0f; }
   __device__ __forceinline__ static float identity() { return CUDART_INF_F; }
   __device__ __forceinline__ static float better(float m, float acc) { return (m < acc) ? m : acc; }
