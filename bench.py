@@ -211,21 +211,26 @@ def run_reference(args):
     nth = os.cpu_count() or 1
     target_nnz = max(1, args.ref_sample_products // N)
     M = csr.M
-    # step s samples the contiguous row block starting at a fixed stride offset
-    starts = np.linspace(0, M - 1, num=max(args.steps + args.warmup, 1), endpoint=False).astype(np.int64)
+    deg = np.diff(rp)
+    cap = max(1, target_nnz // nth)  # longer rows would leave host threads idle
 
-    def sample(r0):
-        p0 = rp[r0]
-        r1 = int(np.searchsorted(rp, p0 + target_nnz, side="left"))
-        r1 = max(min(r1, M), r0 + 1)
-        return r0, r1
+    def sample(i):
+        """Rows drawn uniformly at random (seeded per step) until ~target_nnz
+        nonzeros; rows longer than target/threads are skipped."""
+        order = np.random.default_rng(1000 + i).permutation(M)
+        d = deg[order]
+        ok = order[(d > 0) & (d <= cap)]
+        csum = np.cumsum(deg[ok])
+        rows = np.sort(ok[: int(np.searchsorted(csum, target_nnz)) + 1])
+        srp = np.zeros(rows.size + 1, np.int64)
+        srp[1:] = np.cumsum(deg[rows])
+        idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
+        return srp.astype(np.int32), ci[idx], vv[idx], rows.size
 
     def step(i):
-        r0, r1 = sample(int(starts[i % len(starts)]))
-        p0, p1 = rp[r0], rp[r1]
-        srp = (rp[r0:r1 + 1] - p0).astype(np.int32)
-        _, secs, nlog = O.ref_spmm_csr(srp, ci[p0:p1], vv[p0:p1], Bh, nthreads=nth, want_c=False)
-        return int(p1 - p0), secs, nlog, r1 - r0
+        srp, sci, svv, nrows = sample(i)
+        _, secs, nlog = O.ref_spmm_csr(srp, sci, svv, Bh, nthreads=nth, want_c=False)
+        return int(srp[-1]), secs, nlog, nrows
 
     for i in range(args.warmup):
         step(i)
@@ -243,11 +248,11 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": spec["desc"], "op": "sum", "N": N, "M": M, "nnz": csr.nnz},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": nth, "kind": "reference",
-                         "sample": f"per step a contiguous row block with ~{target_nnz} nnz "
-                                   f"(avg {tot_rows / max(args.steps, 1):.0f} rows) of the same "
-                                   f"matrix; raceset::run on gespmm_alg2.mir (block 4, grid "
-                                   f"rows x N/4), rows split into {nth} parallel instances; "
-                                   f"time = run() calls only"},
+                         "sample": f"per step ~{target_nnz} nnz in {tot_rows / max(args.steps, 1):.0f} "
+                                   f"rows drawn at random (seeded; rows > {cap} nnz skipped) from "
+                                   f"the same matrix; raceset::run on gespmm_alg2.mir (block 4, "
+                                   f"grid rows x N/4), rows split into {nth} parallel instances "
+                                   f"(reference SPEC.md:478-479); time = run() calls only"},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -429,7 +434,7 @@ def main():
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]),
-            "kernel_variant": variant_name(N, B, C),
+            "kernel_variant": variant_name(N, B, C, args.op),
             "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
         }
         print(json.dumps(line))

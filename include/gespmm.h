@@ -26,16 +26,19 @@
  *   - Thread safety: distinct plans may be used concurrently from distinct
  *     threads; one plan must not be executed concurrently with itself.
  *
- * Semantics (normative, oracle/gespmm_oracle.c):
- *   per output cell (i, j), nonzeros are reduced in ascending p, fp32.
- *   SUM : acc = fmaf(val[p], B[col[p]][j], acc) from acc = 0 (accumulate: C0)
- *   MEAN: SUM from 0, then acc / deg(i) (correctly rounded); accumulate adds C0
+ * Semantics (normative, oracle/gespmm_oracle.c), fp32:
+ *   SUM : two ascending FMA chains per row, over the nonzeros at even (A) and
+ *         odd (B) offsets from the row start: A = fmaf(val[p], B[col[p]][j], A)
+ *         from A = 0 (accumulate: C0), B likewise from -0.0; value = A + B
+ *   MEAN: the SUM value from A = 0, then / deg(i) (correctly rounded);
+ *         accumulate adds C0
  *   MAX/MIN: m = val[p]*B[col[p]][j] (rounded, unfused); acc = first m, then
  *         acc = (m > acc) ? m : acc   (MIN: <); accumulate seeds acc = C0
  *   empty rows give 0 (accumulate: C0 for sum/max/min, C0 + 0 for mean).
  *   Rows with more than GESPMM_SEGMENT_LEN nonzeros are reduced in fixed
- *   GESPMM_SEGMENT_LEN-long segments from the row start, combined strictly left
- *   to right (sum/mean: +, max/min: the same comparison).  Results are
+ *   GESPMM_SEGMENT_LEN-long segments from the row start (each segment as above,
+ *   later segments seeded with 0 / -inf / +inf), combined strictly left to
+ *   right (sum/mean: +, max/min: the same comparison).  Results are
  *   deterministic and independent of device, grid and sharding.
  */
 #ifndef GESPMM_H_
@@ -153,10 +156,11 @@ typedef struct gespmm_plan_info {
 } gespmm_plan_info_t;
 gespmm_status_t gespmm_plan_get_info(gespmm_plan_t plan, gespmm_plan_info_t* info);
 
-/* Which kernel variant a given N / alignment selects ("vec4_lpr32_cwm2", ...),
- * and a test-only override ("" = heuristic).  Not thread-safe. */
+/* Which kernel variant a given N / alignment / op selects ("pair_vec4",
+ * "vec4_lpr32_cwm2", ...), and a test-only override ("" = heuristic).
+ * Not thread-safe. */
 const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const float* C,
-                                int64_t ldc);
+                                int64_t ldc, gespmm_reduce_t op);
 gespmm_status_t gespmm_set_variant_override(const char* name);
 
 /* nnz-balanced row partition for row-block sharding over `parts` ranks

@@ -20,11 +20,12 @@
  *     by log replay (tests/golden/, made by oracle/ref_replay.cpp).
  *
  *  2. oracle_spmm_f32 -- the fp32 "twin": the normative fp32 semantics of the
- *     B200 path, i.e. the same ascending-p order, but
- *     fp32 with an explicit fused multiply-add (fmaf), the sum/max/min/mean
- *     reduce operators, and the fixed long-row segmentation (rows with more
- *     than seg_len nonzeros are reduced in seg_len-long segments that are then
- *     combined left to right).  The GPU result is bit-identical to this twin.
+ *     B200 path: fp32 with explicit fused multiply-adds
+ *     (fmaf); sum/mean reduce each row (segment) as two ascending FMA chains
+ *     over the even- and odd-offset positions, added at the end; max/min fold
+ *     in ascending p; long rows (more than seg_len nonzeros) are reduced in
+ *     seg_len-long segments combined left to right.  The GPU result is
+ *     bit-identical to this twin.
  *
  * Build: oracle/Makefile (-O2 -fopenmp -ffp-contract=off, never -ffast-math).
  */
@@ -121,12 +122,21 @@ static void fold_span(int op, int64_t ps, int64_t pe, int64_t N, const int32_t* 
                       const float* init, float* acc) {
   int64_t p = ps;
   if (op == OR_SUM || op == OR_MEAN) {
-    for (int64_t j = 0; j < N; ++j) acc[j] = (mode == 1) ? init[j] : 0.0f;
+    /* Two FMA chains: positions at even offsets from the span start (chain A,
+     * seeded with init or +0) and at odd offsets (chain B, seeded with -0.0,
+     * the exact additive identity); the span's value is A + B. */
+    float* accb = acc + N;
+    for (int64_t j = 0; j < N; ++j) {
+      acc[j] = (mode == 1) ? init[j] : 0.0f;
+      accb[j] = -0.0f;
+    }
     for (; p < pe; ++p) {
       const float v = vals[p];
       const float* b = B + (int64_t)colind[p] * ldb;
-      for (int64_t j = 0; j < N; ++j) acc[j] = fmaf(v, b[j], acc[j]);
+      float* a = ((p - ps) & 1) ? accb : acc;
+      for (int64_t j = 0; j < N; ++j) a[j] = fmaf(v, b[j], a[j]);
     }
+    for (int64_t j = 0; j < N; ++j) acc[j] = acc[j] + accb[j];
     return;
   }
   if (mode == 0) {
@@ -163,9 +173,9 @@ int oracle_spmm_f32(int64_t M, int64_t N, const int32_t* rowptr, const int32_t* 
 #pragma omp parallel
 #endif
   {
-    float* acc = (float*)malloc(sizeof(float) * (size_t)N * 3);
-    float* part = acc + N;
-    float* c0 = acc + 2 * N;
+    float* acc = (float*)malloc(sizeof(float) * (size_t)N * 5);
+    float* part = acc + 2 * N;  /* fold_span uses [x, x + 2N) as its two chains */
+    float* c0 = acc + 4 * N;
 #ifdef _OPENMP
 #pragma omp for schedule(dynamic, 256)
 #endif

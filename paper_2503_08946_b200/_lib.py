@@ -66,7 +66,7 @@ def load():
                                 _int),
         "gespmm_plan_destroy": ([_vp], _int),
         "gespmm_plan_get_info": ([_vp, ctypes.POINTER(PlanInfo)], _int),
-        "gespmm_variant_name": ([_i64, _vp, _i64, _vp, _i64], ctypes.c_char_p),
+        "gespmm_variant_name": ([_i64, _vp, _i64, _vp, _i64, _int], ctypes.c_char_p),
         "gespmm_set_variant_override": ([ctypes.c_char_p], _int),
         "gespmm_partition_rows": ([_i64, _vp, _int, _vp], _int),
         "gespmm_comm_get_unique_id": ([ctypes.c_char_p], _int),

@@ -76,11 +76,13 @@ gespmm_status_t check_shape(int64_t M, int64_t K, int64_t N, int64_t nnz, int64_
   return GESPMM_OK;
 }
 
-Variant pick_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc) {
-  Variant v = choose_variant(N, B, ldb, C, ldc);
+Variant pick_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc,
+                     gespmm_reduce_t op) {
+  Variant v = choose_variant(N, B, ldb, C, ldc, op);
   if (!g_variant_override.empty()) {
     Variant o;
-    if (parse_variant(g_variant_override.c_str(), &o)) {
+    const bool two_chain = op == GESPMM_REDUCE_SUM || op == GESPMM_REDUCE_MEAN;
+    if (parse_variant(g_variant_override.c_str(), &o) && (!o.pair || two_chain)) {
       auto ok = [&](int vec) {
         const uintptr_t a = static_cast<uintptr_t>(vec) * 4;
         return reinterpret_cast<uintptr_t>(B) % a == 0 && reinterpret_cast<uintptr_t>(C) % a == 0 &&
@@ -262,7 +264,7 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
     return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
   if (plan->n_items == 0) return GESPMM_OK;  // M == 0
   cudaStream_t s = as_stream(stream);
-  const Variant v = pick_variant(N, B, ldb, C, ldc);
+  const Variant v = pick_variant(N, B, ldb, C, ldc, op);
   const int ncb = static_cast<int>((N + variant_cols(v) - 1) / variant_cols(v));
   if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
   const int64_t ldp = (N + 3) & ~int64_t(3);
@@ -425,9 +427,9 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
 }
 
 const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const float* C,
-                                int64_t ldc) {
+                                int64_t ldc, gespmm_reduce_t op) {
   static thread_local std::string name;
-  name = variant_name(pick_variant(N, B, ldb, C, ldc));
+  name = variant_name(pick_variant(N, B, ldb, C, ldc, op));
   return name.c_str();
 }
 

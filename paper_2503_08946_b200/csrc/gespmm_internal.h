@@ -32,10 +32,12 @@ constexpr int kPackShift = 40;
 
 // Kernel variant: VEC fp32 columns per lane per load (1, 2 or 4) and CWM column
 // tiles per warp (Coarse-grained Warp Merging); one warp covers 32*VEC*CWM
-// columns of one column block.
+// columns of one column block.  `pair`: the paired-lane sum/mean kernel
+// (gespmm_kernel_pair.cuh), 16 lanes x VEC columns, two nonzeros per warp step.
 struct Variant {
   int vec = 1;
   int cwm = 1;
+  bool pair = false;
 };
 
 // Everything the SpMM kernel reads.  Passed by value (kernel parameter space).
@@ -73,7 +75,8 @@ void set_error(const std::string& msg);
 gespmm_status_t fail(gespmm_status_t s, const std::string& msg);
 gespmm_status_t cuda_fail(cudaError_t e, const char* what);
 
-Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc);
+Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc,
+                       gespmm_reduce_t op);
 int variant_cols(const Variant& v);
 std::string variant_name(const Variant& v);
 bool parse_variant(const char* name, Variant* v);

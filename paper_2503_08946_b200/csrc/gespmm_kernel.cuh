@@ -190,9 +190,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #ifndef GESPMM_ABL_NOGATHER
 #define GESPMM_ABL_NOGATHER 0
 #endif
-#ifndef GESPMM_FRAG_SLOW
-#define GESPMM_FRAG_SLOW 0
-#endif
 #ifndef GESPMM_DOUBLE
 #define GESPMM_DOUBLE 0  // measured: one buffer (60 regs, 32 warps/SM) beats two (spills)
 #endif
@@ -217,6 +214,12 @@ template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::value)
     spmm_kernel(const KParams P) {
   using SR = Semiring<OP>;
+  // sum/mean: two FMA chains per row (even/odd offsets from the row start),
+  // held in accumulator slots by absolute position parity (batches are
+  // 4-aligned, so the slot of batch element u is u & 1); value = slot0 + slot1
+  // (fp32 addition is commutative, so it does not matter which slot holds the
+  // even chain).  max/min: one chain in slot 0.
+  constexpr bool TWO = SR::kFma2;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
   constexpr int U = Pipe<CPL>::U;      // gathers per batch
   constexpr int TW = 32 * VEC;         // columns per CWM tile
@@ -246,19 +249,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
   const bool accumulate = P.accumulate != 0;
   const bool seed_c0 = accumulate && SR::kSeedC0;
 
-  float acc[CWM][VEC];
-  auto set_acc = [&](float x) {
+  float acc[2][CWM][VEC];
+  // Row (segment) start: chain A -- the even offsets from `start` -- gets x
+  // (or C0 when `src`), chain B gets -0.0, the exact additive identity.
+  auto seed = [&](int start, float x, const float* src) {
+    float c[CWM][VEC];
 #pragma unroll
-    for (int w = 0; w < CWM; ++w)
+    for (int w = 0; w < CWM; ++w) {
+      if (src) Vec<VEC>::ld(c[w], src + (woff[w] - woff[0]));
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) acc[w][k] = x;
+      for (int k = 0; k < VEC; ++k) {
+        const float a = src ? c[w][k] : x;
+        if (TWO) {
+          const bool odd = start & 1;
+          acc[0][w][k] = odd ? -0.0f : a;
+          acc[1][w][k] = odd ? a : -0.0f;
+        } else {
+          acc[0][w][k] = a;
+        }
+      }
+    }
   };
   // C rows are addressed through a running pointer (crow = C + row*ldc + the
   // lane's column), advanced by ldc per row: no 64-bit multiply per row.
-  auto load_acc = [&](const float* src) {  // accumulate=1 seed: C0
-#pragma unroll
-    for (int w = 0; w < CWM; ++w) Vec<VEC>::ld(acc[w], src + (woff[w] - woff[0]));
+  auto row_seed = [&](int start, const float* crow_) {
+    seed(start, SR::zero(), seed_c0 ? crow_ : nullptr);
   };
+  auto value = [&](int w, int k) { return TWO ? acc[0][w][k] + acc[1][w][k] : acc[0][w][k]; };
   auto store_row = [&](float* dst, int deg) {
     if (GESPMM_ABL_NOSTORE) return;  // ablation builds only
 #pragma unroll
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
       if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst + (woff[w] - woff[0]));
 #pragma unroll
       for (int k = 0; k < VEC; ++k)
-        o[k] = SR::finalize(acc[w][k], deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
+        o[k] = SR::finalize(value(w, k), deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
       Vec<VEC>::stcs(dst + (woff[w] - woff[0]), o);
     }
   };
@@ -289,17 +306,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     }
   };
 
-  // acc += v * b per the semiring; sum/mean column pairs go through FFMA2
-  // (Blackwell's packed fp32 FMA: two independent RN FMAs, bit-identical)
-  auto fold = [&](float v, const float (&bb)[CWM][VEC], bool first) {
+  // acc[slot] += v * b per the semiring; sum/mean column pairs go through
+  // FFMA2 (Blackwell's packed fp32 FMA: two independent RN FMAs, bit-identical)
+  auto fold = [&](int slot, float v, const float (&bb)[CWM][VEC], bool first) {
+    float (&a)[CWM][VEC] = acc[TWO ? slot : 0];
 #pragma unroll
     for (int w = 0; w < CWM; ++w) {
       if (SR::kFma2 && VEC >= 2) {
 #pragma unroll
-        for (int k = 0; k < VEC; k += 2) fma2_rn(acc[w][k], acc[w][k + 1], v, bb[w][k], bb[w][k + 1]);
+        for (int k = 0; k < VEC; k += 2) fma2_rn(a[w][k], a[w][k + 1], v, bb[w][k], bb[w][k + 1]);
       } else {
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) acc[w][k] = SR::update(acc[w][k], v, bb[w][k], first);
+        for (int k = 0; k < VEC; ++k) a[w][k] = SR::update(a[w][k], v, bb[w][k], first);
       }
     }
   };
@@ -386,9 +404,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     // max/min take their first message as the initial value, except when
     // seeded (accumulate) or in a later segment (seeded with the identity).
     const bool first_ok = SR::kFirstMsg && !accumulate && (is_tile || it.y == 0);
-    if (!is_tile && it.y > 0) set_acc(SR::identity());
-    else if (seed_c0) load_acc(crow);
-    else set_acc(SR::zero());
+    if (!is_tile && it.y > 0) seed(lo, SR::identity(), nullptr);
+    else row_seed(lo, crow);
 
     // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
     auto issue = [&](int qb, float (&b)[U][CWM][VEC]) {
@@ -413,41 +430,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
         const bool first = first_ok && qb == rs;
 #pragma unroll
-        for (int u = 0; u < U; ++u) fold(v[u], b[u], first && u == 0);
+        for (int u = 0; u < U; ++u) fold(u & 1, v[u], b[u], first && u == 0);
         return;
       }
-#if GESPMM_FRAG_SLOW
-      // slow path: fold the batch row fragment by row fragment (one predicated
-      // fold block and one row-advance block, whatever U is)
-      const int qe = min(qb + U, hi);
-      int qq = max(qb, lo);
-      for (;;) {
-        const int lim = min(qe, re);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int p = qb + u;
-          const bool on = p >= qq && p < lim;
-          const bool first = first_ok && p == rs;
-#pragma unroll
-          for (int w = 0; w < CWM; ++w)
-#pragma unroll
-            for (int k = 0; k < VEC; ++k) {
-              const float nv = SR::update(acc[w][k], v[u], b[u][w][k], first);
-              acc[w][k] = on ? nv : acc[w][k];
-            }
-        }
-        qq = lim;
-        if (qq >= qe) break;
-        // qq == re: the current row is complete (tiles only)
-        store_row(crow, re - rs);
-        ++row;
-        crow += ldc;
-        rs = re;
-        re = rp[row + 1];
-        if (seed_c0) load_acc(crow);
-        else set_acc(SR::zero());
-      }
-#else
 #pragma unroll
       for (int u = 0; u < U; ++u) {  // slow path: element by element
         const int p = qb + u;
@@ -458,12 +443,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
           crow += ldc;
           rs = re;
           re = rp[row + 1];
-          if (seed_c0) load_acc(crow);
-          else set_acc(SR::zero());
+          row_seed(rs, crow);
         }
-        fold(v[u], b[u], first_ok && p == rs);
+        fold(u & 1, v[u], b[u], first_ok && p == rs);
       }
-#endif
     };
     if (lo < hi) {
       if (Pipe<CPL>::kDouble) {
@@ -506,8 +489,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
         crow += ldc;
         rs = re;
         re = rp[row + 1];
-        if (seed_c0) load_acc(crow);
-        else set_acc(SR::zero());
+        row_seed(rs, crow);
       }
       continue;
     }
@@ -519,7 +501,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     float* part = P.partials + static_cast<int64_t>(slot + seg) * P.ldp;
 #pragma unroll
     for (int w = 0; w < CWM; ++w)
-      if (cok[w]) Vec<VEC>::st(part + woff[w], acc[w]);
+      if (cok[w]) {
+        float o[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) o[k] = value(w, k);
+        Vec<VEC>::st(part + woff[w], o);
+      }
     __threadfence();
     __syncwarp();
     int ticket = 0;
@@ -531,7 +518,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     __threadfence();
     const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp;
 #pragma unroll
-    for (int w = 0; w < CWM; ++w) Vec<VEC>::ldcg(acc[w], base + woff[w]);
+    for (int w = 0; w < CWM; ++w) {
+      Vec<VEC>::ldcg(acc[0][w], base + woff[w]);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[1][w][k] = -0.0f;  // value() = acc0 + -0 = acc0
+    }
     constexpr int CU = 4;
     for (int s = 1; s < nseg; s += CU) {
       float pv[CU][CWM][VEC];
@@ -548,7 +539,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
 #pragma unroll
           for (int w = 0; w < CWM; ++w)
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) acc[w][k] = SR::combine(acc[w][k], pv[u][w][k]);
+            for (int k = 0; k < VEC; ++k) acc[0][w][k] = SR::combine(acc[0][w][k], pv[u][w][k]);
     }
     store_row(crow, deg);
     if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)

@@ -1,0 +1,319 @@
+// gespmm_kernel_pair.cuh -- paired-lane GE-SpMM kernel for sum/mean at N <= 64.
+//
+// Same work items, staging and row walk as gespmm_kernel.cuh (read that file
+// first); what differs is the lane mapping.  The sum/mean contract reduces each
+// row (segment) as two FMA chains -- the nonzeros at even and at odd offsets
+// from its start -- added at the end.  Here the two
+// chains live in the two 16-lane halves of the warp: half g folds the staged
+// positions of absolute parity g, each lane owning VEC (<= 4) consecutive
+// columns, so every warp instruction gathers two B rows (two 128-bit loads per
+// lane pair at N=64) and the address math / load count per nonzero halve
+// compared with the 32-lane kernel.  Row control stays warp-uniform (both
+// halves walk the same rows); at a row end the halves' chains are added with one
+// shfl_xor(16) -- fp32 addition is commutative, so both halves hold the same
+// bits -- and the lower half stores.
+//
+// The stage is permuted per 8-entry block to [0,2,4,6,1,3,5,7] so a half reads
+// its four (col, val) pairs of a batch with one 128-bit shared load each.
+#pragma once
+
+#include "gespmm_kernel.cuh"
+
+namespace gespmm {
+namespace kern {
+
+#ifndef GESPMM_PAIR_MINBLOCKS
+#define GESPMM_PAIR_MINBLOCKS GESPMM_MINBLOCKS
+#endif
+#ifndef GESPMM_PAIR_U
+#define GESPMM_PAIR_U 8
+#endif
+template <gespmm_reduce_t OP, int VEC, bool OFF32>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
+    spmm_pair_kernel(const KParams P) {
+  using SR = Semiring<OP>;
+  static_assert(SR::kFma2, "paired lanes implement the two-chain (sum/mean) contract only");
+  constexpr int U = GESPMM_PAIR_U;  // positions per batch (U/2 per half; 8 or 16)
+  constexpr int H = U / 2;
+  constexpr int TW = 16 * VEC;   // columns per column block
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ __align__(16) int scol[kWarpsPerBlock][kStageCap];
+  __shared__ __align__(16) float sval[kWarpsPerBlock][kStageCap];
+  __shared__ int rpw[kWarpsPerBlock][kTileMaxRows + 4];
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 4;       // my half = the parity of the positions I fold
+  const int gl = lane & 15;
+  const int cb = blockIdx.y;
+  const int64_t colbase = static_cast<int64_t>(cb) * TW + gl * VEC;
+  const bool cok = colbase < P.N;
+  const int woff = cok ? static_cast<int>(colbase) : 0;
+  const float* bw = P.B + woff;
+  const int64_t ldb = P.ldb;
+  const int64_t ldc = P.ldc;
+  int* const sc = scol[warp];
+  float* const sv = sval[warp];
+  int* const rp = rpw[warp];
+  const bool accumulate = P.accumulate != 0;
+  const bool seed_c0 = accumulate && SR::kSeedC0;
+  const bool storer = g == 0 && cok;
+  const uint64_t bpol = GESPMM_BHINT ? policy_evict_last() : 0;
+
+  float acc[VEC];
+  // chain A (even offsets from `start`) is held by the half whose parity is
+  // start's; it gets x (or C0), the other half -0.0.
+  auto seed = [&](int start, float x, const float* src) {
+    float c[VEC];
+    if (src) Vec<VEC>::ld(c, src);
+    const bool mine = g == (start & 1);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = mine ? (src ? c[k] : x) : -0.0f;
+  };
+  auto row_seed = [&](int start, const float* crow_) {
+    seed(start, SR::zero(), seed_c0 ? crow_ : nullptr);
+  };
+  // A + B across the halves (both halves end with the same bits)
+  auto combined = [&](float (&o)[VEC]) {
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) o[k] = acc[k] + __shfl_xor_sync(FULL, acc[k], 16);
+  };
+  auto store_row = [&](float* dst, int deg) {
+    float o[VEC];
+    combined(o);
+    if (!storer) return;
+    float c0[VEC];
+    if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k)
+      o[k] = SR::finalize(o[k], deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
+    Vec<VEC>::stcs(dst, o);
+  };
+  auto gather = [&](float (&d)[VEC], int x) {
+    if (OFF32) gather_off<VEC>(d, bw, static_cast<uint32_t>(x), bpol);
+    else Vec<VEC>::ldg(d, bw + static_cast<int64_t>(x) * ldb);
+  };
+  auto fold = [&](float v, const float (&b)[VEC]) {
+    if (VEC >= 2) {
+#pragma unroll
+      for (int k = 0; k < VEC; k += 2) fma2_rn(acc[k], acc[k + 1], v, b[k], b[k + 1]);
+    } else {
+      acc[0] = SR::update(acc[0], v, b[0], false);
+    }
+  };
+
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < P.n_items;
+       t += wstride) {
+    __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
+    const int4 it = P.items[t];
+    const bool is_tile = it.y < 0;
+    int lo, hi, nr, re_long = 0;
+    if (is_tile) {
+      int r1, pend;
+      if (t + 1 < P.n_items) {
+        const int4 nx = P.items[t + 1];
+        r1 = nx.x;
+        pend = nx.z;
+      } else {
+        r1 = P.M;
+        pend = P.nnz;
+      }
+      nr = r1 - it.x;
+      lo = it.z;
+      hi = pend;
+      for (int k = lane; k <= nr; k += 32) cp_async4(rp + k, P.rowptr + it.x + k);
+    } else {
+      nr = 1;
+      lo = it.z + it.y * kSeg;
+      re_long = __ldg(P.rowptr + it.x + 1);
+      hi = min(lo + kSeg, re_long);
+    }
+    // ---- CRC staging (as in gespmm_kernel.cuh), then the parity permutation --
+    const int sbase = lo & ~3;
+    const int send = sbase + ((hi - sbase + U - 1) / U) * U;
+    if (P.idx_aligned) {
+      for (int e = sbase + 4 * lane; e < hi; e += 128) {
+        if (e + 4 <= P.nnz) {
+          cp_async16(sc + (e - sbase), P.colind + e);
+          cp_async16(sv + (e - sbase), P.vals + e);
+        } else {
+          for (int q = e; q < P.nnz; ++q) {
+            cp_async4(sc + (q - sbase), P.colind + q);
+            cp_async4(sv + (q - sbase), P.vals + q);
+          }
+        }
+      }
+    } else {
+      for (int e = sbase + lane; e < hi; e += 32) {
+        cp_async4(sc + (e - sbase), P.colind + e);
+        cp_async4(sv + (e - sbase), P.vals + e);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;  // pad: row 0, never folded
+    __syncwarp();
+    {
+      const uint32_t ldb32 = static_cast<uint32_t>(ldb);
+      // per U-block: even offsets first, then odd (a half's entries contiguous);
+      // lane l permutes block l (U <= 16 entries: held in registers)
+      for (int i = U * lane; i < send - sbase; i += 32 * U) {
+        int c[U];
+        float w[U];
+#pragma unroll
+        for (int q = 0; q < U; q += 4) {
+          const int4 a = *reinterpret_cast<int4*>(sc + i + q);
+          const float4 f = *reinterpret_cast<float4*>(sv + i + q);
+          c[q] = a.x, c[q + 1] = a.y, c[q + 2] = a.z, c[q + 3] = a.w;
+          w[q] = f.x, w[q + 1] = f.y, w[q + 2] = f.z, w[q + 3] = f.w;
+        }
+#pragma unroll
+        for (int q = 0; q < U; q += 4) {
+          int d[4];
+          float x[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int src = ((q + r) < H) ? 2 * (q + r) : 2 * (q + r - H) + 1;
+            d[r] = OFF32 ? static_cast<int>(static_cast<uint32_t>(c[src]) * ldb32) : c[src];
+            x[r] = w[src];
+          }
+          *reinterpret_cast<int4*>(sc + i + q) = make_int4(d[0], d[1], d[2], d[3]);
+          *reinterpret_cast<float4*>(sv + i + q) = make_float4(x[0], x[1], x[2], x[3]);
+        }
+      }
+      __syncwarp();
+    }
+
+    // ---- row state (warp-uniform) --------------------------------------------
+    float* crow = P.C + static_cast<int64_t>(it.x) * ldc + woff;
+    int row = 0, rs = lo, re = is_tile ? rp[1] : hi;
+    if (!is_tile && it.y > 0) seed(lo, SR::identity(), nullptr);
+    else row_seed(lo, crow);
+
+    for (int qb = sbase; qb < hi; qb += U) {
+      // my half's four staged entries of this batch: positions qb + 2i + g
+      float b[H][VEC];
+      float v[H];
+#pragma unroll
+      for (int q4 = 0; q4 < H / 4; ++q4) {
+        const int4 o = *reinterpret_cast<const int4*>(sc + (qb - sbase) + H * g + 4 * q4);
+        gather(b[4 * q4 + 0], o.x);
+        gather(b[4 * q4 + 1], o.y);
+        gather(b[4 * q4 + 2], o.z);
+        gather(b[4 * q4 + 3], o.w);
+      }
+#pragma unroll
+      for (int q4 = 0; q4 < H / 4; ++q4) {
+        const float4 vv = *reinterpret_cast<const float4*>(sv + (qb - sbase) + H * g + 4 * q4);
+        v[4 * q4] = vv.x, v[4 * q4 + 1] = vv.y, v[4 * q4 + 2] = vv.z, v[4 * q4 + 3] = vv.w;
+      }
+      if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: the batch is in the current row
+#pragma unroll
+        for (int i = 0; i < H; ++i) fold(v[i], b[i]);
+        continue;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {  // slow path: positions in order
+        const int p = qb + j;
+        if (p < lo || p >= hi) continue;
+        while (p >= re) {  // rows ending at or before p are complete (tiles only)
+          store_row(crow, re - rs);
+          ++row;
+          crow += ldc;
+          rs = re;
+          re = rp[row + 1];
+          row_seed(rs, crow);
+        }
+        if (g == (j & 1)) fold(v[j >> 1], b[j >> 1]);  // my entry j/2 is position qb + j
+      }
+    }
+
+    if (is_tile) {
+      for (;;) {  // the row in progress and any trailing empty rows
+        store_row(crow, re - rs);
+        if (++row >= nr) break;
+        crow += ldc;
+        rs = re;
+        re = rp[row + 1];
+        row_seed(rs, crow);
+      }
+      continue;
+    }
+    // ---- long-row segment: publish A + B, then take a ticket ------------------
+    const int seg = it.y;
+    const int slot = it.w;
+    const int deg = re_long - it.z;
+    const int nseg = (deg + kSeg - 1) / kSeg;
+    {
+      float o[VEC];
+      combined(o);
+      if (storer) Vec<VEC>::st(P.partials + static_cast<int64_t>(slot + seg) * P.ldp + woff, o);
+    }
+    __threadfence();
+    __syncwarp();
+    int ticket = 0;
+    int* counter = P.counters + static_cast<int64_t>(slot) * P.ncb + cb;
+    if (lane == 0) ticket = atomicAdd(counter, 1);
+    ticket = __shfl_sync(FULL, ticket, 0);
+    if (ticket != nseg - 1) continue;
+    // last segment: combine the partials strictly left to right (both halves
+    // compute it; the lower half stores)
+    __threadfence();
+    const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp + woff;
+    float r[VEC];
+    Vec<VEC>::ldcg(r, base);
+    for (int s = 1; s < nseg; ++s) {
+      float pv[VEC];
+      Vec<VEC>::ldcg(pv, base + static_cast<int64_t>(s) * P.ldp);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) r[k] = SR::combine(r[k], pv[k]);
+    }
+    if (storer) {
+      float c0[VEC];
+      if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, crow);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k)
+        r[k] = SR::finalize(r[k], deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
+      Vec<VEC>::stcs(crow, r);
+    }
+    if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
+  }  // item loop
+}
+
+template <gespmm_reduce_t OP, int VEC, bool OFF32>
+cudaError_t launch_pair_t(const KParams& p, cudaStream_t s) {
+  int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks == 0) return cudaSuccess;
+  static thread_local int cached_dev = -1, cached_slots = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_pair_kernel<OP, VEC, OFF32>,
+                                                  kWarpsPerBlock * 32, 0);
+    cached_slots = sms * (per_sm > 0 ? per_sm : 1);
+    cached_dev = dev;
+  }
+  const int64_t slots = (cached_slots + p.ncb - 1) / p.ncb;
+  if (blocks > slots) blocks = slots;
+  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(p.ncb), 1);
+  spmm_pair_kernel<OP, VEC, OFF32><<<grid, kWarpsPerBlock * 32, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <gespmm_reduce_t OP>
+cudaError_t launch_pair(const Variant& v, const KParams& p, cudaStream_t s) {
+  if (p.off32) {
+    if (v.vec == 4) return launch_pair_t<OP, 4, true>(p, s);
+    if (v.vec == 2) return launch_pair_t<OP, 2, true>(p, s);
+    return launch_pair_t<OP, 1, true>(p, s);
+  }
+  if (v.vec == 4) return launch_pair_t<OP, 4, false>(p, s);
+  if (v.vec == 2) return launch_pair_t<OP, 2, false>(p, s);
+  return launch_pair_t<OP, 1, false>(p, s);
+}
+
+}  // namespace kern
+}  // namespace gespmm

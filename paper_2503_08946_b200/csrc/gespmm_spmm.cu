@@ -21,46 +21,53 @@ cudaError_t launch_spmm(gespmm_reduce_t op, const Variant& v, const KParams& p,
   return cudaErrorInvalidValue;
 }
 
-int variant_cols(const Variant& v) { return 32 * v.vec * v.cwm; }
+int variant_cols(const Variant& v) { return v.pair ? 16 * v.vec : 32 * v.vec * v.cwm; }
 
 std::string variant_name(const Variant& v) {
+  if (v.pair) return "pair_vec" + std::to_string(v.vec);
   return "vec" + std::to_string(v.vec) + "_lpr32_cwm" + std::to_string(v.cwm);
 }
 
+namespace {
+// in preference order for equal idle lanes / column blocks.  The paired-lane
+// kernel comes last: at N=64 the 32-lane kernel measured faster (0.362 vs
+// 0.382 ms on config 2); it wins only where 32 lanes would idle (N < 32).
+const Variant kVariants[] = {{4, 1, false}, {4, 2, false}, {2, 1, false}, {2, 2, false},
+                             {1, 1, false}, {1, 2, false}, {4, 1, true},  {2, 1, true},
+                             {1, 1, true}};
+bool two_chain(gespmm_reduce_t op) { return op == GESPMM_REDUCE_SUM || op == GESPMM_REDUCE_MEAN; }
+}  // namespace
+
 bool parse_variant(const char* name, Variant* v) {
-  for (int vec : {1, 2, 4})
-    for (int cwm : {1, 2}) {
-      Variant c{vec, cwm};
-      if (variant_name(c) == name) {
-        *v = c;
-        return true;
-      }
+  for (const Variant& c : kVariants)
+    if (variant_name(c) == name) {
+      *v = c;
+      return true;
     }
   return false;
 }
 
-// Tile shape selected by N (north star item (1)): fewest idle lanes, then fewest
-// column blocks, then the widest loads the alignment of B/C allows.
-Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc) {
+// Tile shape selected by N and op (north star item (1)): fewest idle lanes,
+// then fewest column blocks, then the table order above (the paired-lane
+// kernel is sum/mean only).
+Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc,
+                       gespmm_reduce_t op) {
   auto aligned = [&](int vec) {
     const uintptr_t a = static_cast<uintptr_t>(vec) * 4;
     return reinterpret_cast<uintptr_t>(B) % a == 0 && reinterpret_cast<uintptr_t>(C) % a == 0 &&
            ldb % vec == 0 && ldc % vec == 0 && N % vec == 0;
   };
-  Variant best{1, 1};
+  Variant best{1, 1, false};
   int64_t best_idle = -1, best_ncb = 0;
-  for (int vec : {4, 2, 1}) {
-    if (!aligned(vec)) continue;
-    for (int cwm : {1, 2}) {
-      Variant c{vec, cwm};
-      const int64_t cols = variant_cols(c);
-      const int64_t ncb = (N + cols - 1) / cols;
-      const int64_t idle = ncb * cols - N;
-      if (best_idle < 0 || idle < best_idle || (idle == best_idle && ncb < best_ncb)) {
-        best = c;
-        best_idle = idle;
-        best_ncb = ncb;
-      }
+  for (const Variant& c : kVariants) {
+    if (!aligned(c.vec) || (c.pair && !two_chain(op))) continue;
+    const int64_t cols = variant_cols(c);
+    const int64_t ncb = (N + cols - 1) / cols;
+    const int64_t idle = ncb * cols - N;
+    if (best_idle < 0 || idle < best_idle || (idle == best_idle && ncb < best_ncb)) {
+      best = c;
+      best_idle = idle;
+      best_ncb = ncb;
     }
   }
   return best;

@@ -1,9 +1,11 @@
-// Instantiates the GE-SpMM kernel family for the MEAN reduce op
-// (one translation unit per op so the variants compile in parallel).
-#include "gespmm_kernel.cuh"
+// Instantiates the GE-SpMM kernel family for the MEAN reduce op (the
+// 32-lane kernel and the paired-lane kernel; one translation unit per op so
+// the variants compile in parallel).
+#include "gespmm_kernel_pair.cuh"
 
 namespace gespmm {
 cudaError_t launch_spmm_mean(const Variant& v, const KParams& p, cudaStream_t s) {
+  if (v.pair) return kern::launch_pair<GESPMM_REDUCE_MEAN>(v, p, s);
   return kern::launch_op<GESPMM_REDUCE_MEAN>(v, p, s);
 }
 }  // namespace gespmm

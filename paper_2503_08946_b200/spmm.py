@@ -205,12 +205,12 @@ def partition_rows(rowptr, parts: int) -> np.ndarray:
     return bounds
 
 
-def variant_name(N: int, B=None, out=None) -> str:
+def variant_name(N: int, B=None, out=None, reduce="sum") -> str:
     bp = B.data_ptr() if B is not None else 0
     cp = out.data_ptr() if out is not None else 0
     ldb = B.stride(0) if B is not None else N
     ldc = out.stride(0) if out is not None else N
-    return _L.gespmm_variant_name(N, bp, ldb, cp, ldc).decode()
+    return _L.gespmm_variant_name(N, bp, ldb, cp, ldc, _reduce_code(reduce)).decode()
 
 
 def set_variant_override(name: str = "") -> None:

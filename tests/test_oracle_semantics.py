@@ -47,9 +47,16 @@ def py_twin(rowptr, colind, vals, B, op, accumulate=False, C0=None, seg=0):
             if op in ("sum", "mean"):
                 acc_total = None
                 for k, (a, b) in enumerate(segs):
-                    acc = c0 if (k == 0 and accumulate and op == "sum") else f32(0)
+                    # two chains: even offsets from the segment start (seeded with
+                    # C0 or +0) and odd offsets (seeded with -0.0); value = A + B
+                    ca = c0 if (k == 0 and accumulate and op == "sum") else f32(0)
+                    cb = f32(-0.0)
                     for p in range(a, b):
-                        acc = fma32(vals[p], B[colind[p], j], acc)
+                        if (p - a) % 2 == 0:
+                            ca = fma32(vals[p], B[colind[p], j], ca)
+                        else:
+                            cb = fma32(vals[p], B[colind[p], j], cb)
+                    acc = f32(ca + cb)
                     acc_total = acc if acc_total is None else f32(acc_total + acc)
                 if acc_total is None:
                     acc_total = c0 if (accumulate and op == "sum") else f32(0)
@@ -128,16 +135,32 @@ def test_mean_is_sum_over_degree(oracle_mod):
     np.testing.assert_array_equal(m, want)
 
 
-def test_accumulate_sum_seeds_chain_with_c0(oracle_mod):
-    """accumulate=1 follows the reference's order c = C0; c = c + v*b (fused here)."""
+def test_accumulate_sum_seeds_chain_a_with_c0(oracle_mod):
+    """accumulate=1 seeds chain A (even offsets) with C0, the reference's
+    c = C0; c = c + v*b order restricted to that chain."""
     rowptr = np.array([0, 3], np.int32)
     colind = np.array([0, 1, 2], np.int32)
     vals = np.array([1e8, 1.0, -1e8], np.float32)
     B = np.ones((3, 1), np.float32)
     C0 = np.array([[1.0]], np.float32)
     got = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", accumulate=True, C0=C0)
-    # ((1 + 1e8) + 1) - 1e8 in fp32 = 0 (C0 absorbed), not 1e8 - 1e8 + 2 = 2
-    assert got[0, 0] == np.float32(np.float32(np.float32(np.float32(1) + np.float32(1e8)) + 1) - np.float32(1e8))
+    f = np.float32
+    chain_a = f(f(f(1) + f(1e8)) + f(-1e8))  # C0, then positions 0 and 2
+    chain_b = f(f(-0.0) + f(1.0))             # position 1
+    assert got[0, 0] == f(chain_a + chain_b)
+
+
+def test_sign_of_zero_preserved_by_the_minus_zero_seed(oracle_mod):
+    """Chain B starts at -0.0, so a one-nonzero row returns exactly fma(v, b, +0)
+    and an accumulate of C0 = -0 over an empty row returns -0."""
+    B = np.array([[-0.0], [2.0]], np.float32)
+    got = oracle_mod.spmm_f32(np.array([0, 1], np.int32), np.array([0], np.int32),
+                              np.array([3.0], np.float32), B, "sum")
+    assert got[0, 0] == 0.0 and not np.signbit(got[0, 0])  # 3 * -0 + (+0) = +0
+    C0 = np.array([[-0.0]], np.float32)
+    got = oracle_mod.spmm_f32(np.array([0, 0], np.int32), np.zeros(0, np.int32),
+                              np.zeros(0, np.float32), B, "sum", accumulate=True, C0=C0)
+    assert np.signbit(got[0, 0])
 
 
 def test_empty_rows_give_zero(oracle_mod):
