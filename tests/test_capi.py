@@ -109,7 +109,7 @@ def test_variant_selection_by_N():
     assert variant_name(128) == "vec4_lpr32_cwm1"
     assert variant_name(256) == "vec4_lpr32_cwm2"
     assert variant_name(512) == "vec4_lpr32_cwm2"
-    assert variant_name(33) == "vec1_lpr32_cwm2"
+    assert variant_name(33) == "pair_vec1"  # 3 blocks of 16: 15 idle columns vs 31
     # max/min keep the sequential 32-lane kernel
     assert variant_name(16, reduce="max") == "vec1_lpr32_cwm1"
     assert variant_name(32, reduce="min") == "vec1_lpr32_cwm1"
