@@ -365,6 +365,9 @@ def main():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     t_job = float(t_max.item())  # ms, max over ranks
 
+    from paper_2503_08946_b200.spmm import panel_width
+    pw = panel_width(K, N)
+    n_panels = (N + pw - 1) // pw
     flops = 2.0 * nnz_all * N
     value = flops / (t_job * 1e-3) / 1e9
     U, G = algorithmic_bytes(M_loc, K, N, nnz_loc)
@@ -433,7 +436,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
-            "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]),
+            "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]) * n_panels,
+            "panel_cols": pw,
             "kernel_variant": variant_name(N, B, C, args.op),
             "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
         }

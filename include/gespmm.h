@@ -163,6 +163,16 @@ const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const fl
                                 int64_t ldc, gespmm_reduce_t op);
 gespmm_status_t gespmm_set_variant_override(const char* name);
 
+/* Column-panel width for gespmm_plan_execute (DESIGN.md 5.2 "Panels"): -1 =
+ * heuristic (panels of the widest power-of-two width whose K x width B slab
+ * fits the L2 budget, only when B itself does not), 0 = never split, > 0 =
+ * force panels of `cols` columns.  Results are identical for every width
+ * (columns are independent).  Test/tuning knob; not thread-safe. */
+gespmm_status_t gespmm_set_panel_override(int64_t cols);
+/* The panel width gespmm_plan_execute uses for a K-row B with N columns: one
+ * kernel launch per panel, ceil(N / width) launches per execute. */
+int64_t gespmm_panel_width(int64_t K, int64_t N);
+
 /* nnz-balanced row partition for row-block sharding over `parts` ranks
  * (HOST rowptr): bounds[0..parts] with bounds[0] = 0, bounds[parts] = M,
  * cut so that (nnz + rows) per part is balanced.  Rows never span parts. */

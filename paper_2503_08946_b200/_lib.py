@@ -23,7 +23,8 @@ EXPORTS = [
     "gespmm_version", "gespmm_status_string", "gespmm_last_error", "gespmm_validate_csr",
     "gespmm_validate_csr_device", "gespmm_csr_spmm", "gespmm_csr_spmm_host",
     "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_destroy", "gespmm_plan_get_info",
-    "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_partition_rows",
+    "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_set_panel_override",
+    "gespmm_panel_width", "gespmm_partition_rows",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
 ]
 
@@ -68,6 +69,8 @@ def load():
         "gespmm_plan_get_info": ([_vp, ctypes.POINTER(PlanInfo)], _int),
         "gespmm_variant_name": ([_i64, _vp, _i64, _vp, _i64, _int], ctypes.c_char_p),
         "gespmm_set_variant_override": ([ctypes.c_char_p], _int),
+        "gespmm_set_panel_override": ([_i64], _int),
+        "gespmm_panel_width": ([_i64, _i64], _i64),
         "gespmm_partition_rows": ([_i64, _vp, _int, _vp], _int),
         "gespmm_comm_get_unique_id": ([ctypes.c_char_p], _int),
         "gespmm_comm_init": ([ctypes.POINTER(_vp), _int, ctypes.c_char_p, _int], _int),

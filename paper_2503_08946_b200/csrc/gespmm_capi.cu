@@ -166,6 +166,31 @@ gespmm_status_t host_workspace(int64_t bytes, char** out) {
   return GESPMM_OK;
 }
 
+// Panel width for an N-column product over K B-rows.  GESPMM_PANEL=<cols>
+// overrides (0 = one panel); otherwise a single panel unless K x N x 4 bytes
+// exceeds the L2 budget, then the widest power-of-two panel (>= kMinPanel
+// columns) whose slab fits; no panels when even the narrowest slab does not fit.
+int64_t g_panel_override = [] {
+  const char* e = std::getenv("GESPMM_PANEL");
+  return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(-1);
+}();
+
+int64_t panel_width(int64_t K, int64_t N) {
+  const int64_t forced = g_panel_override;
+  if (forced == 0) return N;
+  if (forced > 0) return forced < N ? forced : N;
+  constexpr int64_t kL2Budget = int64_t(GESPMM_PANEL_L2_MB) << 20;
+  constexpr int64_t kMinPanel = GESPMM_PANEL_MIN;
+  // measured (profiles/r1_panels.txt): Reddit-like K=233K, N=256 -> 64-column
+  // panels (60 MB slabs) 12.47 -> 9.05 ms; R-MAT K=4M, N=128, where even a
+  // 64-column slab (1 GB) exceeds L2, panels only re-stream the CSR (3.04 ->
+  // 3.29 ms): so panel only when the narrowest panel's slab fits.
+  if (K * N * 4 <= kL2Budget || K * kMinPanel * 4 > kL2Budget) return N;
+  int64_t w = 256;
+  while (w > kMinPanel && K * w * 4 > kL2Budget) w /= 2;
+  return w < N ? w : N;
+}
+
 }  // namespace
 }  // namespace gespmm
 
@@ -264,35 +289,44 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
     return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
   if (plan->n_items == 0) return GESPMM_OK;  // M == 0
   cudaStream_t s = as_stream(stream);
-  const Variant v = pick_variant(N, B, ldb, C, ldc, op);
-  const int ncb = static_cast<int>((N + variant_cols(v) - 1) / variant_cols(v));
-  if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
+  // Column panels (DESIGN.md 5.2 "Panels"): when B's row slab K x N does not
+  // fit in L2, the columns are processed in panels of `pw` columns, one launch
+  // per panel on the same stream, so the gathered B working set of each launch
+  // is K x pw and stays L2-resident; colind/vals are re-streamed per panel.
+  // Per-column arithmetic is unchanged (columns are independent).
+  const int64_t pw = panel_width(plan->K, N);
   const int64_t ldp = (N + 3) & ~int64_t(3);
-  st = ensure_workspace(plan, ldp, ncb, s);
-  if (st != GESPMM_OK) return st;
-  KParams p{};
-  p.rowptr = rowptr;
-  p.colind = colind;
-  p.vals = vals;
-  p.B = B;
-  p.C = C;
-  p.ldb = ldb;
-  p.ldc = ldc;
-  p.N = N;
-  p.ldp = ldp;
-  p.items = plan->items;
-  p.n_items = plan->n_items;
-  p.M = static_cast<int>(plan->M);
-  p.nnz = static_cast<int>(plan->nnz);
-  p.partials = plan->partials;
-  p.counters = plan->counters;
-  p.accumulate = accumulate ? 1 : 0;
-  p.ncb = ncb;
-  p.idx_aligned = (reinterpret_cast<uintptr_t>(colind) % 16 == 0) &&
-                  (reinterpret_cast<uintptr_t>(vals) % 16 == 0);
-  p.off32 = plan->K * ldb <= (int64_t(1) << 32);
-  cudaError_t e = launch_spmm(op, v, p, s);
-  if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
+  for (int64_t c0 = 0; c0 < N; c0 += pw) {
+    const int64_t n = N - c0 < pw ? N - c0 : pw;
+    const Variant v = pick_variant(n, B + c0, ldb, C + c0, ldc, op);
+    const int ncb = static_cast<int>((n + variant_cols(v) - 1) / variant_cols(v));
+    if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
+    st = ensure_workspace(plan, ldp, ncb, s);
+    if (st != GESPMM_OK) return st;
+    KParams p{};
+    p.rowptr = rowptr;
+    p.colind = colind;
+    p.vals = vals;
+    p.B = B + c0;
+    p.C = C + c0;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.N = n;
+    p.ldp = ldp;
+    p.items = plan->items;
+    p.n_items = plan->n_items;
+    p.M = static_cast<int>(plan->M);
+    p.nnz = static_cast<int>(plan->nnz);
+    p.partials = plan->partials;
+    p.counters = plan->counters;
+    p.accumulate = accumulate ? 1 : 0;
+    p.ncb = ncb;
+    p.idx_aligned = (reinterpret_cast<uintptr_t>(colind) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(vals) % 16 == 0);
+    p.off32 = plan->K * ldb <= (int64_t(1) << 32);
+    cudaError_t e = launch_spmm(op, v, p, s);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
+  }
   return GESPMM_OK;
 }
 
@@ -431,6 +465,13 @@ const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const fl
   static thread_local std::string name;
   name = variant_name(pick_variant(N, B, ldb, C, ldc, op));
   return name.c_str();
+}
+
+int64_t gespmm_panel_width(int64_t K, int64_t N) { return N < 1 ? 0 : panel_width(K, N); }
+
+gespmm_status_t gespmm_set_panel_override(int64_t cols) {
+  g_panel_override = cols < 0 ? -1 : cols;
+  return GESPMM_OK;
 }
 
 gespmm_status_t gespmm_set_variant_override(const char* name) {

@@ -29,6 +29,14 @@ constexpr int kStageCap = 640;
 static_assert(kTileWork + kSeg + kRowCost + 2 <= kStageCap, "stage too small for the largest item");
 // Low 40 bits of the packed plan scan carry tile work, high 24 bits segment counts.
 constexpr int kPackShift = 40;
+// Column panels: B slabs larger than this are processed in column panels
+// (gespmm_capi.cu panel_width); panels are at least GESPMM_PANEL_MIN columns.
+#ifndef GESPMM_PANEL_L2_MB
+#define GESPMM_PANEL_L2_MB 80
+#endif
+#ifndef GESPMM_PANEL_MIN
+#define GESPMM_PANEL_MIN 64
+#endif
 
 // Kernel variant: VEC fp32 columns per lane per load (1, 2 or 4) and CWM column
 // tiles per warp (Coarse-grained Warp Merging); one warp covers 32*VEC*CWM

@@ -140,6 +140,12 @@ __device__ __forceinline__ void prefetch_off(const float* base, uint32_t off) {
   asm volatile("{\n .reg .u64 a;\n mad.wide.u32 a, %0, 4, %1;\n prefetch.global.L2::evict_last [a];\n}" ::"r"(off),
                "l"(base));
 }
+#ifndef GESPMM_ITEM_PREFETCH
+#define GESPMM_ITEM_PREFETCH 0  // measured: no change (0.364 vs 0.363 ms config 2)
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -330,6 +336,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
        t += wstride) {
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];
+    // the next item's descriptor into L1 (no registers held): its load at the
+    // top of the next iteration then skips a full global-memory latency
+    if (GESPMM_ITEM_PREFETCH && lane == 0 && t + wstride < P.n_items) prefetch_l1(P.items + t + wstride);
     const bool is_tile = it.y < 0;
     // ---- item decode: nonzero span [lo, hi) and its rows --------------------
     // A segment is run as a one-row tile whose row ends at the segment end.

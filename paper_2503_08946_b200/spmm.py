@@ -215,3 +215,13 @@ def variant_name(N: int, B=None, out=None, reduce="sum") -> str:
 
 def set_variant_override(name: str = "") -> None:
     _lib.check(_L.gespmm_set_variant_override(name.encode()))
+
+
+def panel_width(K: int, N: int) -> int:
+    """Columns per kernel launch gespmm_plan_execute uses for K x N."""
+    return int(_L.gespmm_panel_width(int(K), int(N)))
+
+
+def set_panel_override(cols: int = -1) -> None:
+    """Column-panel width: -1 heuristic, 0 never split, > 0 forced width."""
+    _lib.check(_L.gespmm_set_panel_override(int(cols)))

@@ -94,23 +94,38 @@ def rmat_csr(scale: int, edges: int, seed: int = 3, device="cpu", a=0.57, b=0.19
 
 
 def reddit_like_csr(M: int = 232_965, nnz_target: int = 114_615_892, seed: int = 5,
-                    device="cpu", alpha: float = 1.9):
-    """Reddit-shaped graph: power-law (Pareto) degrees scaled to nnz_target,
-    columns uniform per row and deduplicated (torch tensors)."""
+                    device="cpu", alpha: float = 2.2, max_deg: int = 21_657):
+    """Reddit-shaped graph (BASELINE configs[2]): M = 232,965 rows, ~114.6 M
+    nonzeros (mean degree ~492), Pareto(alpha) degrees capped at Reddit's max
+    degree 21,657; columns uniform per row, deduplicated (torch tensors).
+
+    The degree scale is bisected so that the EXPECTED number of unique
+    columns, sum_i M(1 - (1 - 1/M)^deg_i), equals nnz_target: the post-dedup
+    nnz lands within ~0.1% of the target."""
     import torch
 
     dev = torch.device(device)
+    gh = torch.Generator()
+    gh.manual_seed(seed)
+    u = torch.rand(M, generator=gh, dtype=torch.float64)
+    w = (1.0 - u).pow(-1.0 / (alpha - 1.0))
+    lo, hi = 1e-3, 1e9
+    for _ in range(80):
+        s = (lo * hi) ** 0.5
+        d = torch.clamp((w * s).round(), 1, max_deg)
+        uniq = float((M * (1.0 - (1.0 - 1.0 / M) ** d)).sum())
+        if uniq < nnz_target:
+            lo = s
+        else:
+            hi = s
+    deg = torch.clamp((w * hi).round(), 1, max_deg).to(torch.int64).to(dev)
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
-    u = torch.rand(M, generator=g, device=dev, dtype=torch.float64)
-    w = (1.0 - u).pow(-1.0 / (alpha - 1.0))
-    deg = torch.clamp((w / w.sum() * nnz_target).round().to(torch.int64), 1, M)
-    rowptr = torch.zeros(M + 1, dtype=torch.int64, device=dev)
-    rowptr[1:] = torch.cumsum(deg, 0)
-    nnz = int(rowptr[-1])
+    nnz = int(deg.sum())
     rows = torch.repeat_interleave(torch.arange(M, device=dev), deg)
     cols = torch.randint(0, M, (nnz,), generator=g, device=dev)
     key = torch.unique(rows * M + cols)
+    del rows, cols
     rows = key // M
     colind = (key % M).to(torch.int32)
     counts = torch.bincount(rows, minlength=M)

@@ -115,6 +115,28 @@ def test_accumulate_bit_exact(cuda, oracle_mod, op):
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("N,panel", [(256, 64), (100, 32), (200, 64), (64, 16)])
+@pytest.mark.parametrize("op", OPS)
+def test_column_panels_bit_exact(cuda, oracle_mod, op, N, panel):
+    """Column panels (one launch per panel) give the same bits as one launch."""
+    from paper_2503_08946_b200 import spmm
+
+    rng = np.random.default_rng(31 + N)
+    M, K = 600, 350
+    rowptr, colind, vals = random_csr(rng, M, K, 0.04, long_rows=[(7, 1300), (8, 257)], empty_frac=0.3)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    spmm.set_panel_override(panel)
+    try:
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        got_acc, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op, C0=C0)
+    finally:
+        spmm.set_panel_override(-1)
+    np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+    np.testing.assert_array_equal(
+        got_acc, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG))
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("op", ["sum", "max"])
 def test_every_variant_bit_exact(cuda, oracle_mod, variant, op):
