@@ -2,7 +2,7 @@
 "SpMM GFLOP/s (2*nnz*N) and achieved HBM GB/s vs roofline at 1/2/4/8 B200").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload config2|config1|config3-N|config4] [--op sum|max|min|mean]
+                    [--workload config2|config1|config3-N|config4|config5] [--op sum|max|min|mean]
 
 Workload (default, BASELINE configs[1]): R-MAT scale 20 (1M rows), 16M edges
 requested (Graph500 a/b/c = .57/.19/.19, deduplicated), x dense B with N=64,
@@ -74,6 +74,9 @@ def workload_spec(name):
     if name == "config4":
         return dict(kind="rmat", scale=22, edges=64 * 2**20, N=128, seed=3,
                     desc="R-MAT scale 22 (4M rows), 64M edges requested (dedup), N=128 (configs[3])")
+    if name == "config5":
+        return dict(kind="rmat", scale=24, edges=2**30, N=128, seed=3,
+                    desc="R-MAT scale 24 (16M rows), 2^30 edges requested (dedup), N=128 (configs[4], one GPU)")
     if name == "config1":
         return dict(kind="uniform", M=4096, K=4096, density=0.01, N=32, seed=1,
                     desc="uniform 4096x4096, 1% density, N=32 (configs[0])")
@@ -84,13 +87,20 @@ def workload_spec(name):
     raise SystemExit(f"unknown workload {name}")
 
 
-def make_workload(spec, device):
+def make_workload(spec, device, native=True):
+    """native=True: the library's CUDA generators (gespmm_rmat_csr /
+    gespmm_uniform_fill); the reference arm passes native=False and gets the
+    same recursion from torch ops, so no libgespmm code runs on that arm."""
     import numpy as np
     import torch
 
     from paper_2503_08946_b200 import workloads as W
 
-    if spec["kind"] == "rmat":
+    native = native and device.type == "cuda"
+    if spec["kind"] == "rmat" and native:
+        # native CUDA generator (gespmm_rmat_csr: Philox keys, CUB sort + unique)
+        csr = W.rmat_csr_gpu(spec["scale"], spec["edges"], seed=spec["seed"], device=device)
+    elif spec["kind"] == "rmat":
         csr = W.rmat_csr(spec["scale"], spec["edges"], seed=spec["seed"], device=device)
     elif spec["kind"] == "uniform":
         c = W.uniform_csr(spec["M"], spec["K"], spec["density"], seed=spec["seed"])
@@ -98,7 +108,10 @@ def make_workload(spec, device):
                     torch.as_tensor(c.vals, device=device), c.M, c.K)
     else:
         csr = W.reddit_like_csr(seed=spec["seed"], device=device)
-    B = W.dense_torch(csr.K, spec["N"], seed=2, device=device)
+    if native:
+        B = W.dense_gpu(csr.K, spec["N"], seed=2, device=device)
+    else:
+        B = W.dense_torch(csr.K, spec["N"], seed=2, device=device)
     del np
     return csr, B
 
@@ -202,7 +215,7 @@ def run_reference(args):
                           "unavailable": "oracle/_ref/libgespmm_ref.so not built (reference tree absent at build time)"}))
         return 0
     dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
-    csr, B = make_workload(spec, dev)
+    csr, B = make_workload(spec, dev, native=False)
     N = spec["N"]
     rp = csr.rowptr.cpu().numpy().astype(np.int64)
     ci = csr.colind.cpu().numpy()

@@ -179,6 +179,21 @@ int64_t gespmm_panel_width(int64_t K, int64_t N);
 gespmm_status_t gespmm_partition_rows(int64_t M, const int32_t* rowptr, int parts,
                                       int64_t* bounds);
 
+/* ---- synthetic inputs on the GPU ------------
+ * R-MAT (Graph500 quadrant recursion with probabilities a, b, c, d = 1-a-b-c;
+ * no vertex permutation) with 2^scale rows/cols and `edges` sampled edges,
+ * deduplicated and sorted by (row, col), as CSR into caller DEVICE buffers:
+ * rowptr int32[2^scale + 1], colind int32[edges], vals fp32[edges] (U[-1,1)).
+ * *nnz_out = unique edges (<= edges).  Uniforms are Philox4x32-10 keyed by
+ * `seed` and counted by (edge, level): the graph depends on the arguments only.
+ * Synchronizes `stream` once (the unique count). */
+gespmm_status_t gespmm_rmat_csr(int32_t scale, int64_t edges, double a, double b, double c,
+                                uint64_t seed, int32_t* rowptr, int32_t* colind, float* vals,
+                                int64_t* nnz_out, void* stream);
+/* out[i] = lo + (hi - lo) * u_i, u_i = Philox(seed, i) in [0, 1) (24-bit), on `stream`. */
+gespmm_status_t gespmm_uniform_fill(float* out, int64_t n, float lo, float hi, uint64_t seed,
+                                    void* stream);
+
 /* ---- multi-GPU (row-block sharding) -------------
  * NCCL is resolved at run time (dlopen "libnccl.so.2"; the copy already loaded
  * in the process wins), so the library never drags in a second NCCL. */

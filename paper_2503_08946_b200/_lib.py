@@ -25,6 +25,7 @@ EXPORTS = [
     "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_destroy", "gespmm_plan_get_info",
     "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_set_panel_override",
     "gespmm_panel_width", "gespmm_partition_rows",
+    "gespmm_rmat_csr", "gespmm_uniform_fill",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
 ]
 
@@ -72,6 +73,9 @@ def load():
         "gespmm_set_panel_override": ([_i64], _int),
         "gespmm_panel_width": ([_i64, _i64], _i64),
         "gespmm_partition_rows": ([_i64, _vp, _int, _vp], _int),
+        "gespmm_rmat_csr": ([_int, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                             ctypes.c_uint64, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp], _int),
+        "gespmm_uniform_fill": ([_vp, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_uint64, _vp], _int),
         "gespmm_comm_get_unique_id": ([ctypes.c_char_p], _int),
         "gespmm_comm_init": ([ctypes.POINTER(_vp), _int, ctypes.c_char_p, _int], _int),
         "gespmm_comm_destroy": ([_vp], _int),

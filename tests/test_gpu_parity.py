@@ -350,6 +350,59 @@ def test_config2_full_size_bit_exact(cuda, oracle_mod, op):
     np.testing.assert_array_equal(got.cpu().numpy(), want)
 
 
+def sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3000, seed=0):
+    """Checks C on a sample of rows (the longest rows, random rows, the first
+    and last rows) against the twin, bit for bit, without moving the full B to
+    the host: each sampled row's result depends only on its own nonzeros and
+    the B rows they name, so the sub-problem uses a compacted B."""
+    import torch
+
+    rp = csr.rowptr.long()
+    deg = (rp[1:] - rp[:-1])
+    M = csr.M
+    g = torch.Generator(device="cpu")
+    g.manual_seed(seed)
+    rows = torch.cat([torch.topk(deg, min(16, M)).indices.cpu(), torch.randint(0, M, (n_random,), generator=g),
+                      torch.tensor([0, M - 1])]).unique().to(rp.device)
+    sdeg = deg[rows]
+    srp = torch.zeros(rows.numel() + 1, dtype=torch.int64, device=rp.device)
+    srp[1:] = torch.cumsum(sdeg, 0)
+    pos = torch.repeat_interleave(rp[rows], sdeg) + (
+        torch.arange(int(srp[-1]), device=rp.device) - torch.repeat_interleave(srp[:-1], sdeg))
+    cols = csr.colind.long()[pos]
+    ucols, inv = torch.unique(cols, return_inverse=True)
+    want = oracle_mod.spmm_f32(srp.int().cpu().numpy(), inv.int().cpu().numpy(),
+                               csr.vals[pos].cpu().numpy(), B[ucols].cpu().numpy(), op, seg_len=SEG)
+    np.testing.assert_array_equal(C[rows].cpu().numpy(), want)
+    return int(rows.numel()), int(srp[-1])
+
+
+@pytest.mark.parametrize("workload", ["config4", "config5", "config3"])
+def test_full_size_configs_sampled_bit_exact(cuda, oracle_mod, workload):
+    """BASELINE configs 3-5 at full size (R-MAT scale 22/64M and scale 24/2^30
+    edges with N=128, Reddit-like 114.6M nnz with N=256 in column panels) on one
+    GPU: every op bit-exact to the twin on sampled rows incl. the longest rows."""
+    import torch
+
+    from paper_2503_08946_b200 import workloads as W
+    from paper_2503_08946_b200.spmm import Plan
+
+    if workload == "config3":
+        csr = W.reddit_like_csr(device=cuda)
+        N = 256
+    else:
+        scale, edges = (22, 64 * 2**20) if workload == "config4" else (24, 2**30)
+        csr = W.rmat_csr_gpu(scale, edges, seed=3, device=cuda)
+        N = 128
+    B = W.dense_gpu(csr.K, N, seed=2, device=cuda)
+    plan = Plan(csr.rowptr, csr.colind, csr.K)
+    C = torch.empty((csr.M, N), dtype=torch.float32, device=cuda)
+    for op in OPS:
+        plan.execute(csr.vals, B, op, out=C)
+        torch.cuda.synchronize()
+        sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=2000 if workload == "config5" else 3000)
+
+
 def test_reference_side_cpp_adapter(cuda, tmp_path):
     """The C++ binding a raceset maintainer adds (examples/raceset_adapter.cpp,
     linked against the reference's own library) computes the shipped instance
