@@ -419,8 +419,9 @@ def main():
                "h2d_bytes_per_step": int(4 * (M_loc + 1) + 8 * nnz_loc + 4 * K * N),
                "d2h_bytes_per_step": int(4 * M_loc * N),
                "ms_per_step": float(e2e_t.item()) * 1e3,
-               "path": "gespmm_csr_spmm_host (pinned host buffers; H2D, device CSR validation, "
-                       "plan, kernel, D2H; wall clock per call)"}
+               "path": "gespmm_csr_spmm_host (pinned host buffers; pipelined: rowptr + B H2D, "
+                       "plan, then per row chunk colind/vals H2D -> device colind check -> kernel "
+                       "-> C rows D2H overlapping the next chunk; wall clock per call)"}
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
     cpu = None

@@ -20,6 +20,11 @@ namespace gespmm {
 gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* colind,
                            bool check_colind, cudaStream_t s);
 gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K, cudaStream_t s);
+cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc, int64_t* d_ranges,
+                         cudaStream_t s);
+cudaError_t validate_colind_async(const int* colind, int64_t p0, int64_t p1, int64_t K, int* err,
+                                  cudaStream_t s);
+std::string csr_error_message(int err, int64_t K);
 
 namespace {
 thread_local std::string g_last_error;
@@ -34,15 +39,18 @@ static double now_ms() {
       .count();
 }
 
+// GESPMM_TRACE=1: synchronize at each mark (device phase times);
+// GESPMM_TRACE=2: host timestamps only (where the host thread blocks).
 Trace::Trace(const char* s) : scope(s) {
   const char* e = std::getenv("GESPMM_TRACE");
   on = e && *e && *e != '0';
+  sync = on && *e != '2';
   if (on) t0 = last = now_ms();
 }
 
 void Trace::mark(const char* phase, cudaStream_t stream) {
   if (!on) return;
-  cudaStreamSynchronize(stream);
+  if (sync) cudaStreamSynchronize(stream);
   const double t = now_ms();
   std::fprintf(stderr, "[gespmm trace] %s %-24s %8.3f ms (total %8.3f)\n", scope, phase, t - last,
                t - t0);
@@ -124,23 +132,37 @@ std::mutex& host_ws_mutex() {
   return m;
 }
 
-// Side stream + event for the host entry point's copies, one per device.
-gespmm_status_t side_stream(cudaStream_t* s, cudaEvent_t* ev) {
-  struct Side {
-    cudaStream_t s = nullptr;
-    cudaEvent_t ev = nullptr;
-  };
-  static Side side[64];
+// The host entry point's plan, one per device, re-planned in place per call.
+gespmm_plan_s* host_plan() {
+  static gespmm_plan_s* plans[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  Side& x = side[dev & 63];
-  if (!x.s) {
-    cudaError_t e = cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_fail(e, "side stream");
+  gespmm_plan_s*& p = plans[dev & 63];
+  if (!p) {
+    p = new gespmm_plan_s();
+    p->device = dev;
   }
-  *s = x.s;
-  *ev = x.ev;
+  return p;
+}
+
+// Copy streams + events of the pipelined host entry point, one set per device.
+struct Pipe {
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaEvent_t ev[2 + 2 * kMaxChunks] = {};
+};
+gespmm_status_t pipe_streams(Pipe** out) {
+  static Pipe pipes[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Pipe& x = pipes[dev & 63];
+  if (!x.in) {
+    cudaError_t e = cudaStreamCreateWithFlags(&x.in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x.out, cudaStreamNonBlocking);
+    for (auto& ev : x.ev)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline streams");
+  }
+  *out = &x;
   return GESPMM_OK;
 }
 
@@ -189,6 +211,56 @@ int64_t panel_width(int64_t K, int64_t N) {
   int64_t w = 256;
   while (w > kMinPanel && K * w * 4 > kL2Budget) w /= 2;
   return w < N ? w : N;
+}
+
+// The launches of one execute (one per column panel), optionally restricted
+// to the item range *range (device memory) with an on-device abort flag.
+gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* rowptr,
+                              const int32_t* colind, const float* vals, const float* B, int64_t ldb,
+                              float* C, int64_t ldc, gespmm_reduce_t op, int accumulate,
+                              const int64_t* range, const int* abort_flag, cudaStream_t s) {
+  gespmm_status_t st = GESPMM_OK;
+  // Column panels (DESIGN.md 5.2 "Panels"): when B's row slab K x N does not
+  // fit in L2, the columns are processed in panels of `pw` columns, one launch
+  // per panel on the same stream, so the gathered B working set of each launch
+  // is K x pw and stays L2-resident; colind/vals are re-streamed per panel.
+  // Per-column arithmetic is unchanged (columns are independent).
+  const int64_t pw = panel_width(plan->K, N);
+  const int64_t ldp = (N + 3) & ~int64_t(3);
+  for (int64_t c0 = 0; c0 < N; c0 += pw) {
+    const int64_t n = N - c0 < pw ? N - c0 : pw;
+    const Variant v = pick_variant(n, B + c0, ldb, C + c0, ldc, op);
+    const int ncb = static_cast<int>((n + variant_cols(v) - 1) / variant_cols(v));
+    if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
+    st = ensure_workspace(plan, ldp, ncb, s);
+    if (st != GESPMM_OK) return st;
+    KParams p{};
+    p.rowptr = rowptr;
+    p.colind = colind;
+    p.vals = vals;
+    p.B = B + c0;
+    p.C = C + c0;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.N = n;
+    p.ldp = ldp;
+    p.items = plan->items;
+    p.n_items = plan->n_items;
+    p.M = static_cast<int>(plan->M);
+    p.nnz = static_cast<int>(plan->nnz);
+    p.partials = plan->partials;
+    p.counters = plan->counters;
+    p.accumulate = accumulate ? 1 : 0;
+    p.ncb = ncb;
+    p.idx_aligned = (reinterpret_cast<uintptr_t>(colind) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(vals) % 16 == 0);
+    p.off32 = plan->K * ldb <= (int64_t(1) << 32);
+    p.range = range;
+    p.abort_flag = abort_flag;
+    cudaError_t e = launch_spmm(op, v, p, s);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
+  }
+  return GESPMM_OK;
 }
 
 }  // namespace
@@ -288,46 +360,8 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
   if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
     return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
   if (plan->n_items == 0) return GESPMM_OK;  // M == 0
-  cudaStream_t s = as_stream(stream);
-  // Column panels (DESIGN.md 5.2 "Panels"): when B's row slab K x N does not
-  // fit in L2, the columns are processed in panels of `pw` columns, one launch
-  // per panel on the same stream, so the gathered B working set of each launch
-  // is K x pw and stays L2-resident; colind/vals are re-streamed per panel.
-  // Per-column arithmetic is unchanged (columns are independent).
-  const int64_t pw = panel_width(plan->K, N);
-  const int64_t ldp = (N + 3) & ~int64_t(3);
-  for (int64_t c0 = 0; c0 < N; c0 += pw) {
-    const int64_t n = N - c0 < pw ? N - c0 : pw;
-    const Variant v = pick_variant(n, B + c0, ldb, C + c0, ldc, op);
-    const int ncb = static_cast<int>((n + variant_cols(v) - 1) / variant_cols(v));
-    if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
-    st = ensure_workspace(plan, ldp, ncb, s);
-    if (st != GESPMM_OK) return st;
-    KParams p{};
-    p.rowptr = rowptr;
-    p.colind = colind;
-    p.vals = vals;
-    p.B = B + c0;
-    p.C = C + c0;
-    p.ldb = ldb;
-    p.ldc = ldc;
-    p.N = n;
-    p.ldp = ldp;
-    p.items = plan->items;
-    p.n_items = plan->n_items;
-    p.M = static_cast<int>(plan->M);
-    p.nnz = static_cast<int>(plan->nnz);
-    p.partials = plan->partials;
-    p.counters = plan->counters;
-    p.accumulate = accumulate ? 1 : 0;
-    p.ncb = ncb;
-    p.idx_aligned = (reinterpret_cast<uintptr_t>(colind) % 16 == 0) &&
-                    (reinterpret_cast<uintptr_t>(vals) % 16 == 0);
-    p.off32 = plan->K * ldb <= (int64_t(1) << 32);
-    cudaError_t e = launch_spmm(op, v, p, s);
-    if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
-  }
-  return GESPMM_OK;
+  return execute_range(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, nullptr,
+                       nullptr, as_stream(stream));
 }
 
 gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
@@ -378,86 +412,160 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   g_last_error.clear();
   gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
   if (st != GESPMM_OK) return st;
+  if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
+  if ((M > 0 && !rowptr) || (nnz > 0 && (!colind || !vals)) || (K * N > 0 && !B) || (M * N > 0 && !C))
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
+  // The rowptr contract (reference src/oracle.cpp:302-307): its ends here,
+  // monotonicity by the plan build on the device (before any launch); colind
+  // range on the device per chunk, before that chunk's launch.
+  if (M > 0 && rowptr[0] != 0) return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr[0] must be 0");
+  if ((M > 0 ? static_cast<int64_t>(rowptr[M]) : 0) != nnz)
+    return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr end differs from nnz of colInd");
+  if (M == 0 || N == 0) return GESPMM_OK;
   cudaStream_t s = as_stream(stream);
-  // Device staging: one grow-only workspace per device, reused across calls
-  // (a fresh 0.7 GB allocation per call costs more than the kernel).
+  // One grow-only device workspace per device, reused across calls (a fresh
+  // 0.7 GB allocation per call costs more than the kernel).
   std::lock_guard<std::mutex> lock(host_ws_mutex());
   Trace tr("host");
   auto al = [](int64_t bytes) { return (bytes + 255) & ~int64_t(255); };
   const int64_t b_rp = al((M + 1) * 4), b_ci = al(nnz * 4), b_v = al(nnz * 4),
-                b_B = al(K * N * 4), b_C = al(M * N * 4);
+                b_B = al(K * N * 4), b_C = al(M * N * 4), b_x = al(8 * (kMaxChunks + 1) + 64);
   char* ws = nullptr;
-  st = host_workspace(b_rp + b_ci + b_v + b_B + b_C, &ws);
+  st = host_workspace(b_rp + b_ci + b_v + b_B + b_C + b_x, &ws);
   if (st != GESPMM_OK) return st;
-  tr.mark("workspace", s);
   auto* d_rp = reinterpret_cast<int32_t*>(ws);
   auto* d_ci = reinterpret_cast<int32_t*>(ws + b_rp);
   auto* d_v = reinterpret_cast<float*>(ws + b_rp + b_ci);
   auto* d_B = reinterpret_cast<float*>(ws + b_rp + b_ci + b_v);
   auto* d_C = reinterpret_cast<float*>(ws + b_rp + b_ci + b_v + b_B);
-  cudaError_t e = cudaSuccess;
-  auto h2d = [&](void* d, const void* h, size_t n) {
-    if (e == cudaSuccess && n) e = cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s);
-  };
-  // The structure goes first on `s`; vals, B (and C0) go on a side stream so
-  // the plan build (which synchronizes `s`) overlaps their transfer.
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t ev = nullptr;
-  st = side_stream(&s2, &ev);
+  auto* d_ranges = reinterpret_cast<int64_t*>(ws + b_rp + b_ci + b_v + b_B + b_C);
+  auto* d_err = reinterpret_cast<int*>(d_ranges + kMaxChunks + 1);
+  Pipe* pp = nullptr;
+  st = pipe_streams(&pp);
   if (st != GESPMM_OK) return st;
-  if (std::getenv("GESPMM_NO_SIDE_STREAM")) s2 = s;  // debug switch
-  cudaEvent_t ev0 = nullptr;
-  e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventRecord(ev0, s);  // s2 must not overtake prior work on s
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, ev0, 0);
-  if (ev0) cudaEventDestroy(ev0);
-  h2d(d_rp, rowptr, static_cast<size_t>(M + 1) * 4);
-  h2d(d_ci, colind, static_cast<size_t>(nnz) * 4);
-  auto h2d2 = [&](void* d, const void* h, size_t n) {
-    if (e == cudaSuccess && n) e = cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s2);
+  cudaStream_t s_in = pp->in, s_out = pp->out;
+  tr.mark("workspace", s);
+
+  // Row chunks: contiguous rows with ~equal nnz + rows; C rows of chunk c go
+  // back to the host as soon as chunk c's launch is done, while chunk c+1's
+  // colind/vals are still arriving (PCIe is full duplex).  Chunks need >= ~8 MB
+  // of C each to amortize their launches and copies.
+  const int64_t c_bytes = M * N * 4;
+  int nc = static_cast<int>(c_bytes / (8 << 20));
+  if (nc > kMaxChunks) nc = kMaxChunks;
+  if (nc < 1 || std::getenv("GESPMM_HOST_NO_PIPELINE")) nc = 1;
+  int64_t rows[kMaxChunks + 1];
+  rows[0] = 0;
+  rows[nc] = M;
+  for (int c = 1; c < nc; ++c) {  // first row whose (nnz + rows) prefix reaches c/nc of the total
+    const double target = static_cast<double>(nnz + M) * c / nc;
+    int64_t lo = rows[c - 1], hi = M;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (static_cast<double>(rowptr[mid]) + static_cast<double>(mid) < target) lo = mid + 1;
+      else hi = mid;
+    }
+    rows[c] = lo;
+  }
+  // A launch over chunk c's items can read up to kStageCap + 4 nonzeros past
+  // rowptr[rows[c+1]] (a tile that starts in chunk c and runs into chunk c+1,
+  // plus the 16-byte staging granule): chunk c's transfer covers that overhang.
+  const int64_t overhang = kStageCap + 4;
+  auto pos_end = [&](int c) {
+    const int64_t p = static_cast<int64_t>(rowptr[rows[c + 1]]) + (c + 1 < nc ? overhang : 0);
+    return p < nnz ? p : nnz;
   };
-  h2d2(d_v, vals, static_cast<size_t>(nnz) * 4);
-  if (e == cudaSuccess && K * N > 0) {
-    if (ldb == N) h2d2(d_B, B, static_cast<size_t>(K * N) * 4);
-    else e = cudaMemcpy2DAsync(d_B, N * 4, B, ldb * 4, N * 4, K, cudaMemcpyHostToDevice, s2);
+
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  // ---- host -> device on s_in: rowptr, B (and C0), then colind/vals per chunk
+  chk(cudaEventRecord(pp->ev[0], s));  // s_in must not overtake prior work on s
+  chk(cudaStreamWaitEvent(s_in, pp->ev[0], 0));
+  chk(cudaMemcpyAsync(d_rp, rowptr, static_cast<size_t>(M + 1) * 4, cudaMemcpyHostToDevice, s_in));
+  chk(cudaEventRecord(pp->ev[1], s_in));  // rowptr resident
+  if (K > 0) {
+    if (ldb == N) chk(cudaMemcpyAsync(d_B, B, static_cast<size_t>(K * N) * 4, cudaMemcpyHostToDevice, s_in));
+    else chk(cudaMemcpy2DAsync(d_B, N * 4, B, ldb * 4, N * 4, K, cudaMemcpyHostToDevice, s_in));
   }
-  if (e == cudaSuccess && accumulate && M * N > 0) {
-    if (ldc == N) h2d2(d_C, C, static_cast<size_t>(M * N) * 4);
-    else e = cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s2);
+  if (accumulate) {
+    if (ldc == N) chk(cudaMemcpyAsync(d_C, C, static_cast<size_t>(M * N) * 4, cudaMemcpyHostToDevice, s_in));
+    else chk(cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s_in));
   }
-  if (e == cudaSuccess) e = cudaEventRecord(ev, s2);
+  int64_t sent = 0;
+  for (int c = 0; c < nc; ++c) {
+    const int64_t p1 = pos_end(c);
+    if (p1 > sent) {
+      chk(cudaMemcpyAsync(d_ci + sent, colind + sent, static_cast<size_t>(p1 - sent) * 4,
+                          cudaMemcpyHostToDevice, s_in));
+      chk(cudaMemcpyAsync(d_v + sent, vals + sent, static_cast<size_t>(p1 - sent) * 4,
+                          cudaMemcpyHostToDevice, s_in));
+      sent = p1;
+    }
+    chk(cudaEventRecord(pp->ev[2 + c], s_in));  // chunk c's nonzeros resident
+  }
   if (e != cudaSuccess) {
-    cudaStreamSynchronize(s2);
+    cudaStreamSynchronize(s_in);
     return cuda_fail(e, "host to device copy");
   }
-  gespmm_plan_t plan = nullptr;
-  st = gespmm_plan_create(&plan, M, K, nnz, d_rp, d_ci, 1, stream);
-  if (st != GESPMM_OK) {
-    cudaStreamSynchronize(s2);
-    return st;
+  tr.mark("H2D issued", s);
+  // ---- plan from rowptr (overlaps the B transfer), chunk item ranges --------
+  chk(cudaStreamWaitEvent(s, pp->ev[1], 0));
+  chk(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  // The plan object is cached per device with the workspace and re-planned in
+  // place: no cudaMalloc/cudaFree per call (cudaFree synchronizes the device
+  // and costs milliseconds at these sizes).
+  gespmm_plan_s* plan = host_plan();
+  plan->M = M;
+  plan->K = K;
+  plan->nnz = nnz;
+  if (e == cudaSuccess) st = build_plan(plan, d_rp, nullptr, false, s);
+  if (e != cudaSuccess || st != GESPMM_OK) {
+    cudaStreamSynchronize(s_in);
+    return e != cudaSuccess ? cuda_fail(e, "plan") : st;
   }
-  tr.mark("structure H2D + plan", s);
-  e = cudaStreamWaitEvent(s, ev, 0);
-  if (e != cudaSuccess) {
-    cudaStreamSynchronize(s2);
-    gespmm_plan_destroy(plan);
-    return cuda_fail(e, "stream join");
+  chk(chunk_ranges(plan, rows, nc, d_ranges, s));
+  tr.mark("rowptr H2D + plan", s);
+  // ---- per chunk: colind check, the launch(es), C rows back on s_out --------
+  for (int c = 0; c < nc && e == cudaSuccess; ++c) {
+    const int64_t p0 = c == 0 ? 0 : pos_end(c - 1);
+    chk(cudaStreamWaitEvent(s, pp->ev[2 + c], 0));
+    chk(validate_colind_async(d_ci, p0, pos_end(c), K, d_err, s));
+    if (e != cudaSuccess) break;
+    st = execute_range(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate,
+                       nc > 1 ? d_ranges + c : nullptr, d_err, s);
+    if (st != GESPMM_OK) break;
+    chk(cudaEventRecord(pp->ev[2 + kMaxChunks + c], s));
+    chk(cudaStreamWaitEvent(s_out, pp->ev[2 + kMaxChunks + c], 0));
+    const int64_t r0 = rows[c], nr = rows[c + 1] - rows[c];
+    if (nr > 0) {
+      if (ldc == N)
+        chk(cudaMemcpyAsync(C + r0 * N, d_C + r0 * N, static_cast<size_t>(nr * N) * 4,
+                            cudaMemcpyDeviceToHost, s_out));
+      else
+        chk(cudaMemcpy2DAsync(C + r0 * ldc, ldc * 4, d_C + r0 * N, N * 4, N * 4, nr,
+                              cudaMemcpyDeviceToHost, s_out));
+    }
   }
-  tr.mark("values/B H2D (joined)", s);
-  st = gespmm_plan_execute(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate, stream);
-  tr.mark("kernel", s);
-  if (st == GESPMM_OK && M * N > 0) {
-    if (ldc == N)
-      e = cudaMemcpyAsync(C, d_C, static_cast<size_t>(M * N) * 4, cudaMemcpyDeviceToHost, s);
-    else
-      e = cudaMemcpy2DAsync(C, ldc * 4, d_C, N * 4, N * 4, M, cudaMemcpyDeviceToHost, s);
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  tr.mark("C D2H", s);
-  if (st == GESPMM_OK && e != cudaSuccess) st = cuda_fail(e, "device to host copy");
-  gespmm_plan_destroy(plan);
-  tr.mark("plan destroy", s);
-  return st;
+  tr.mark("chunks issued", s);
+  int h_err = 0;
+  chk(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  const cudaError_t e1 = cudaStreamSynchronize(s_out);
+  tr.mark("sync out", s);
+  const cudaError_t e2 = cudaStreamSynchronize(s_in);
+  const cudaError_t e3 = cudaStreamSynchronize(s);
+  chk(e1);
+  chk(e2);
+  chk(e3);
+  tr.mark("chunks + C D2H", s);
+  if (st != GESPMM_OK) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "pipelined host spmm");
+  // C's contents are unspecified after CSR_INVALID (earlier chunks may have
+  // been written back); no launch ever read an out-of-range colind.
+  if (h_err) return fail(GESPMM_CSR_INVALID, csr_error_message(h_err, K));
+  return GESPMM_OK;
 }
 
 const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const float* C,

@@ -38,6 +38,9 @@ constexpr int kPackShift = 40;
 #define GESPMM_PANEL_MIN 64
 #endif
 
+// Pipelined host path: at most this many row chunks per call.
+constexpr int kMaxChunks = 16;
+
 // Kernel variant: VEC fp32 columns per lane per load (1, 2 or 4) and CWM column
 // tiles per warp (Coarse-grained Warp Merging); one warp covers 32*VEC*CWM
 // columns of one column block.  `pair`: the paired-lane sum/mean kernel
@@ -67,12 +70,17 @@ struct KParams {
   int ncb;                 // column blocks (gridDim.y)
   int idx_aligned;         // colind and vals 16-byte aligned -> 128-bit staging loads
   int off32;               // K*ldb <= 2^32: stage 32-bit B-row element offsets
+  // Pipelined host path (gespmm_csr_spmm_host): the launch runs items
+  // [range[0], range[1]) only (nullptr: all), and returns at once when
+  // *abort_flag is set (a failed on-device colind check of an earlier chunk).
+  const int64_t* range;
+  const int* abort_flag;
 };
 
 // GESPMM_TRACE=1: phase timings of the host entry point and the plan build on
 // stderr (each phase is synchronized; diagnostics only).
 struct Trace {
-  bool on = false;
+  bool on = false, sync = false;
   double t0 = 0, last = 0;
   const char* scope = "";
   explicit Trace(const char* s);
@@ -98,6 +106,7 @@ cudaError_t launch_spmm(gespmm_reduce_t op, const Variant& v, const KParams& p,
 struct gespmm_plan_s {
   int64_t M = 0, K = 0, nnz = 0;
   int4* items = nullptr;
+  int64_t items_cap = 0;
   int64_t n_items = 0, n_tiles = 0, n_long = 0, n_segs = 0;
   float* partials = nullptr;
   int64_t partial_floats = 0;

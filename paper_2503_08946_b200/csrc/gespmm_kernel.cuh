@@ -332,13 +332,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
   // a sibling in its CTA finishes a longer item).  Control flow is warp-uniform
   // and the kernel uses no CTA-wide barrier.
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < P.n_items;
+  int64_t t_begin = 0, t_end = P.n_items;
+  if (P.range) {  // one chunk of the pipelined host path
+    if (*reinterpret_cast<const volatile int*>(P.abort_flag)) return;
+    t_begin = P.range[0];
+    t_end = P.range[1];
+  }
+  for (int64_t t = t_begin + static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < t_end;
        t += wstride) {
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];
     // the next item's descriptor into L1 (no registers held): its load at the
     // top of the next iteration then skips a full global-memory latency
-    if (GESPMM_ITEM_PREFETCH && lane == 0 && t + wstride < P.n_items) prefetch_l1(P.items + t + wstride);
+    if (GESPMM_ITEM_PREFETCH && lane == 0 && t + wstride < t_end) prefetch_l1(P.items + t + wstride);
     const bool is_tile = it.y < 0;
     // ---- item decode: nonzero span [lo, hi) and its rows --------------------
     // A segment is run as a one-row tile whose row ends at the segment end.

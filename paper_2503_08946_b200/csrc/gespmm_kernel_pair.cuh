@@ -103,7 +103,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
   };
 
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < P.n_items;
+  int64_t t_begin = 0, t_end = P.n_items;
+  if (P.range) {  // one chunk of the pipelined host path
+    if (*reinterpret_cast<const volatile int*>(P.abort_flag)) return;
+    t_begin = P.range[0];
+    t_end = P.range[1];
+  }
+  for (int64_t t = t_begin + static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < t_end;
        t += wstride) {
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];

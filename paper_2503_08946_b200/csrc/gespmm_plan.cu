@@ -119,7 +119,54 @@ std::string csr_error_text(int err, int64_t K) {
   return "invalid csr";
 }
 
+struct ChunkRows {
+  int64_t r[kMaxChunks + 1];
+};
+
+// ranges[c] = first item whose row is >= rows[c] (items are in row order; a
+// long row's segment 0 precedes its other segments), ranges[nc] = n_items.
+__global__ void k_chunk_ranges(const int4* __restrict__ items, int64_t n_items, ChunkRows rows, int nc,
+                               int64_t* __restrict__ ranges) {
+  const int c = threadIdx.x;
+  if (c > nc) return;
+  if (c == nc) {
+    ranges[c] = n_items;
+    return;
+  }
+  int64_t lo = 0, hi = n_items;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (items[mid].x < rows.r[c]) lo = mid + 1;
+    else hi = mid;
+  }
+  ranges[c] = c == 0 ? 0 : lo;
+}
+
 }  // namespace
+
+cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc, int64_t* d_ranges,
+                         cudaStream_t s) {
+  if (nc < 1 || nc > kMaxChunks) return cudaErrorInvalidValue;
+  ChunkRows cr{};
+  for (int c = 0; c <= nc; ++c) cr.r[c] = rows[c];
+  k_chunk_ranges<<<1, 32, 0, s>>>(plan->items, plan->n_items, cr, nc, d_ranges);
+  return cudaGetLastError();
+}
+
+// Validates colind[p0, p1) on the device, OR-ing an error bit into *err (no sync).
+cudaError_t validate_colind_async(const int* colind, int64_t p0, int64_t p1, int64_t K, int* err,
+                                  cudaStream_t s) {
+  if (p1 <= p0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = (p1 - p0 + 255) / 256;
+  if (blocks > 4 * sms) blocks = 4 * sms;
+  k_colind<<<static_cast<unsigned>(blocks), 256, 0, s>>>(colind + p0, p1 - p0, static_cast<int>(K), err);
+  return cudaGetLastError();
+}
+
+std::string csr_error_message(int err, int64_t K) { return csr_error_text(err, K); }
 
 // Validates colind on the device; returns the error bits via *err_host (sync).
 gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K,
@@ -239,10 +286,17 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
   plan->n_segs = static_cast<int64_t>(h.last_E >> kPackShift) + static_cast<int64_t>(h.last_packed >> kPackShift);
   plan->n_long = h.n_long;
   plan->n_tiles = plan->n_items - plan->n_segs;
-  ce = cudaMalloc(&plan->items, static_cast<size_t>(plan->n_items > 0 ? plan->n_items : 1) * sizeof(int4));
-  if (ce != cudaSuccess) {
-    cudaFreeAsync(arena, s);
-    return cuda_fail(ce, "plan items");
+  if (!plan->items || plan->items_cap < plan->n_items) {  // grow-only (re-planned plans reuse it)
+    if (plan->items) cudaFree(plan->items);
+    plan->items = nullptr;
+    plan->items_cap = 0;
+    const int64_t cap = plan->n_items > 0 ? plan->n_items : 1;
+    ce = cudaMalloc(&plan->items, static_cast<size_t>(cap) * sizeof(int4));
+    if (ce != cudaSuccess) {
+      cudaFreeAsync(arena, s);
+      return cuda_fail(ce, "plan items");
+    }
+    plan->items_cap = cap;
   }
   tr.mark("totals D2H + items alloc", s);
   k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, plan->items);

@@ -299,6 +299,60 @@ def test_host_entry_point(cuda, oracle_mod):
     np.testing.assert_array_equal(got, want)
 
 
+def powerlaw_csr(rng, M, K, mean_deg, long_rows=()):
+    """Vectorized: heavy-tailed degrees (many empty rows), unsorted columns with
+    duplicates, plus the given (row, degree) long rows."""
+    deg = np.minimum((rng.pareto(1.5, M) * mean_deg / 2).astype(np.int64), 4000)
+    deg[rng.random(M) < 0.3] = 0
+    for r, d in long_rows:
+        deg[r] = d
+    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    colind = rng.integers(0, K, int(rowptr[-1])).astype(np.int32)
+    vals = rng.uniform(-1, 1, colind.size).astype(np.float32)
+    return rowptr, colind, vals
+
+
+@pytest.mark.parametrize("op", ["sum", "max", "mean"])
+def test_host_entry_point_pipelined_chunks(cuda, oracle_mod, op):
+    """gespmm_csr_spmm_host at a size where it pipelines row chunks (C >= 16 MB:
+    B first, colind/vals per chunk, C rows back per chunk), long rows and
+    tiles straddling the chunk boundaries; bit-exact to the twin."""
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    rng = np.random.default_rng(40)
+    M, K, N = 150_000, 20_000, 64  # C = 38 MB -> 4 chunks
+    long_rows = [(i * M // 4 + d, 300 + 97 * d) for i in range(1, 4) for d in (-2, -1, 0, 1)]
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 12, long_rows)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, op)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, op, C0=C0)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_host_entry_point_pipelined_invalid_colind(cuda, oracle_mod):
+    """An out-of-range column in a late chunk: CsrInvalid with the reference's
+    message, no launch touches it (no sticky CUDA error), the next call works."""
+    from paper_2503_08946_b200.errors import Error, ErrorKind
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    rng = np.random.default_rng(41)
+    M, K, N = 150_000, 20_000, 64
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 12)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    bad = colind.copy()
+    bad[int(rowptr[-1]) * 3 // 4] = K + 5
+    with pytest.raises(Error) as ei:
+        csr_spmm_host(rowptr, bad, vals, B, "sum")
+    assert ei.value.kind == ErrorKind.CsrInvalid
+    assert f"colInd entry out of [0,{K})" in str(ei.value)
+    got = csr_spmm_host(rowptr, colind, vals, B, "sum")
+    np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG))
+
+
 def test_deterministic_and_shard_invariant(cuda, oracle_mod):
     """Same bits run-to-run, and row-sharded computation (the multi-GPU path's
     per-rank work) reproduces the unsharded result bit for bit."""
