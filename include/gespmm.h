@@ -141,6 +141,20 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
                                     const int32_t* colind, const float* vals, const float* B,
                                     int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
                                     int accumulate, void* stream);
+
+/* One row chunk of an execute (compute overlapped with the
+ * C all-gather / the D2H of finished rows).  Runs the plan's work items whose
+ * first row lies in [row_begin, row_end).  Executing consecutive chunks
+ * [r0=0, r1), [r1, r2), ..., [r_j, r_j+1) in order on ONE stream makes every C
+ * row < r_j+1 final once chunk j has run (a tile that starts before r_j+1 and
+ * runs past it is finished by chunk j); all chunks together equal one
+ * gespmm_plan_execute bit for bit.  Not concurrent with another execute of
+ * the same plan. */
+gespmm_status_t gespmm_plan_execute_rows(gespmm_plan_t plan, int64_t row_begin, int64_t row_end,
+                                         int64_t N, const int32_t* rowptr, const int32_t* colind,
+                                         const float* vals, const float* B, int64_t ldb, float* C,
+                                         int64_t ldc, gespmm_reduce_t op, int accumulate,
+                                         void* stream);
 gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan);
 
 /* Plan introspection (tests, benches). */

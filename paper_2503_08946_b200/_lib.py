@@ -22,7 +22,7 @@ SEGMENT_LEN = 256  # GESPMM_SEGMENT_LEN
 EXPORTS = [
     "gespmm_version", "gespmm_status_string", "gespmm_last_error", "gespmm_validate_csr",
     "gespmm_validate_csr_device", "gespmm_csr_spmm", "gespmm_csr_spmm_host",
-    "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_destroy", "gespmm_plan_get_info",
+    "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_execute_rows", "gespmm_plan_destroy", "gespmm_plan_get_info",
     "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_set_panel_override",
     "gespmm_panel_width", "gespmm_partition_rows",
     "gespmm_rmat_csr", "gespmm_uniform_fill",
@@ -66,6 +66,8 @@ def load():
         "gespmm_plan_create": ([ctypes.POINTER(_vp), _i64, _i64, _i64, _vp, _vp, _int, _vp], _int),
         "gespmm_plan_execute": ([_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _int, _int, _vp],
                                 _int),
+        "gespmm_plan_execute_rows": ([_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
+                                      _int, _int, _vp], _int),
         "gespmm_plan_destroy": ([_vp], _int),
         "gespmm_plan_get_info": ([_vp, ctypes.POINTER(PlanInfo)], _int),
         "gespmm_variant_name": ([_i64, _vp, _i64, _vp, _i64, _int], ctypes.c_char_p),

@@ -22,6 +22,8 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
 gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K, cudaStream_t s);
 cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc, int64_t* d_ranges,
                          cudaStream_t s);
+cudaError_t row_item_range(const gespmm_plan_s* plan, const int64_t* rows, int64_t* d_range,
+                           cudaStream_t s);
 cudaError_t validate_colind_async(const int* colind, int64_t p0, int64_t p1, int64_t K, int* err,
                                   cudaStream_t s);
 std::string csr_error_message(int err, int64_t K);
@@ -364,8 +366,35 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
                        nullptr, as_stream(stream));
 }
 
+gespmm_status_t gespmm_plan_execute_rows(gespmm_plan_t plan, int64_t row_begin, int64_t row_end,
+                                         int64_t N, const int32_t* rowptr, const int32_t* colind,
+                                         const float* vals, const float* B, int64_t ldb, float* C,
+                                         int64_t ldc, gespmm_reduce_t op, int accumulate,
+                                         void* stream) {
+  if (!plan) return fail(GESPMM_INVALID_ARG, "invalid argument: plan is null");
+  gespmm_status_t st = check_shape(plan->M, plan->K, N, plan->nnz, ldb, ldc);
+  if (st != GESPMM_OK) return st;
+  if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
+  if (row_begin < 0 || row_end < row_begin || row_end > plan->M)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: need 0 <= row_begin <= row_end <= M");
+  if (plan->n_items == 0 || row_end == row_begin) return GESPMM_OK;
+  cudaStream_t s = as_stream(stream);
+  if (!plan->row_range) {
+    cudaError_t e = cudaMalloc(&plan->row_range, 4 * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(plan->row_range, 0, 4 * sizeof(int64_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "plan row range");
+  }
+  const int64_t rows[2] = {row_begin, row_end};
+  cudaError_t e = row_item_range(plan, rows, plan->row_range, s);
+  if (e != cudaSuccess) return cuda_fail(e, "row chunk range");
+  return execute_range(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate,
+                       plan->row_range, reinterpret_cast<const int*>(plan->row_range + 2), s);
+}
+
 gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
   if (!plan) return GESPMM_OK;
+  if (plan->row_range) cudaFree(plan->row_range);
   if (plan->items) cudaFree(plan->items);
   if (plan->partials) cudaFree(plan->partials);
   if (plan->counters) cudaFree(plan->counters);

@@ -111,6 +111,7 @@ struct gespmm_plan_s {
   float* partials = nullptr;
   int64_t partial_floats = 0;
   int* counters = nullptr;
+  int64_t* row_range = nullptr;  // [2] items of the current execute_rows chunk (+ a zero abort flag)
   int64_t counter_ints = 0;
   int device = 0;
 };

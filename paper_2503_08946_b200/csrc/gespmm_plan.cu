@@ -125,11 +125,13 @@ struct ChunkRows {
 
 // ranges[c] = first item whose row is >= rows[c] (items are in row order; a
 // long row's segment 0 precedes its other segments), ranges[nc] = n_items.
+// pin = 1 (chunk partitions): ranges[0] = 0 and ranges[nc] = n_items;
+// pin = 0: every entry is the lower bound of rows[c], c < nc.
 __global__ void k_chunk_ranges(const int4* __restrict__ items, int64_t n_items, ChunkRows rows, int nc,
-                               int64_t* __restrict__ ranges) {
+                               int64_t* __restrict__ ranges, int pin) {
   const int c = threadIdx.x;
-  if (c > nc) return;
-  if (c == nc) {
+  if (pin ? c > nc : c >= nc) return;
+  if (pin && c == nc) {
     ranges[c] = n_items;
     return;
   }
@@ -139,7 +141,7 @@ __global__ void k_chunk_ranges(const int4* __restrict__ items, int64_t n_items, 
     if (items[mid].x < rows.r[c]) lo = mid + 1;
     else hi = mid;
   }
-  ranges[c] = c == 0 ? 0 : lo;
+  ranges[c] = (pin && c == 0) ? 0 : lo;
 }
 
 }  // namespace
@@ -149,7 +151,17 @@ cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc,
   if (nc < 1 || nc > kMaxChunks) return cudaErrorInvalidValue;
   ChunkRows cr{};
   for (int c = 0; c <= nc; ++c) cr.r[c] = rows[c];
-  k_chunk_ranges<<<1, 32, 0, s>>>(plan->items, plan->n_items, cr, nc, d_ranges);
+  k_chunk_ranges<<<1, 32, 0, s>>>(plan->items, plan->n_items, cr, nc, d_ranges, 1);
+  return cudaGetLastError();
+}
+
+// d_range[k] = first item whose row is >= rows[k], k = 0, 1 (any row range).
+cudaError_t row_item_range(const gespmm_plan_s* plan, const int64_t* rows, int64_t* d_range,
+                           cudaStream_t s) {
+  ChunkRows cr{};
+  cr.r[0] = rows[0];
+  cr.r[1] = rows[1];
+  k_chunk_ranges<<<1, 32, 0, s>>>(plan->items, plan->n_items, cr, 2, d_range, 0);
   return cudaGetLastError();
 }
 

@@ -68,15 +68,65 @@ def gather_C(C_local, bounds, group=None):
     return full
 
 
+def chunk_bounds(bounds, world: int, chunks: int):
+    """Row chunks of every rank's slab, computable by all ranks from the
+    partition alone: chunk j of rank w is rows [lo, hi) of the GLOBAL matrix,
+    equal row counts."""
+    out = []
+    for w in range(world):
+        a, b = int(bounds[w]), int(bounds[w + 1])
+        out.append([(a + (b - a) * j // chunks, a + (b - a) * (j + 1) // chunks) for j in range(chunks)])
+    return out
+
+
+def gather_C_overlapped(compute_chunk, full, bounds, chunks: int, group=None, cuda_streams=None):
+    """Compute-overlapped C all-gather.  For j = 0..chunks-1
+    every rank computes chunk j of its slab (``compute_chunk(j, lo, hi)``, rows
+    of the global matrix, written into ``full``), then every rank's chunk j is
+    broadcast by its owner while chunk j+1 is computed.  All ranks post the
+    broadcasts in the same (j, owner) order.  ``cuda_streams`` = (compute,
+    comm) torch streams on GPUs; None runs the same schedule synchronously
+    (gloo/CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    cb = chunk_bounds(bounds, world, chunks)
+    for j in range(chunks):
+        lo, hi = cb[rank][j]
+        compute_chunk(j, lo, hi)
+        if cuda_streams is None:
+            for w in range(world):
+                a, b = cb[w][j]
+                if b > a:
+                    dist.broadcast(full[a:b], src=w, group=group)
+            continue
+        comp, comm = cuda_streams
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev)  # this rank's chunk j is final (execute_rows contract)
+            for w in range(world):
+                a, b = cb[w][j]
+                if b > a:
+                    dist.broadcast(full[a:b], src=w, group=group)
+    if cuda_streams is not None:
+        cuda_streams[0].wait_stream(cuda_streams[1])
+    return full
+
+
 class ShardedSpMM:
     """Per-rank driver: owns the rank's row block and its cached Plan.
 
-    ``compute`` defaults to the B200 path (Plan.execute); it is injectable so
-    the host-side sharding logic can be exercised with CPU tensors.
+    ``compute`` / ``compute_rows`` default to the B200 path (Plan.execute /
+    Plan.execute_rows); they are injectable so the host-side sharding logic
+    can be exercised with CPU tensors (gloo).
     """
 
     def __init__(self, rowptr_local, colind_local, K: int, bounds, root: int = 0,
-                 group=None, compute: Optional[Callable] = None):
+                 group=None, compute: Optional[Callable] = None,
+                 compute_rows: Optional[Callable] = None):
         self.rowptr = rowptr_local
         self.colind = colind_local
         self.K = int(K)
@@ -84,16 +134,22 @@ class ShardedSpMM:
         self.root = root
         self.group = group
         self._compute = compute
+        self._compute_rows = compute_rows
+        self._comm_stream = None
         self._plan = None
-        if compute is None:
+        if compute is None and compute_rows is None:
             from .spmm import Plan
 
             self._plan = Plan(rowptr_local, colind_local, K)
 
     def __call__(self, vals_local, B, reduce: str = "sum", gather: bool = False,
-                 broadcast: bool = True):
+                 broadcast: bool = True, chunks: int = 1):
+        """chunks > 1 with gather=True: the C all-gather of chunk j overlaps the
+        computation of chunk j+1 (gather_C_overlapped)."""
         if broadcast:
             broadcast_B(B, self.root, self.group)
+        if gather and chunks > 1 and (self._plan is not None or self._compute_rows is not None):
+            return self._gather_overlapped(vals_local, B, reduce, chunks)
         if self._compute is not None:
             C = self._compute(self.rowptr, self.colind, vals_local, B, reduce)
         else:
@@ -101,3 +157,31 @@ class ShardedSpMM:
         if gather:
             return gather_C(C, self.bounds, self.group)
         return C
+
+    def _gather_overlapped(self, vals_local, B, reduce, chunks):
+        import torch
+        import torch.distributed as dist
+
+        rank = dist.get_rank(self.group)
+        M = int(self.bounds[-1])
+        a = int(self.bounds[rank])
+        N = B.shape[1]
+        full = torch.empty((M, N), dtype=torch.float32, device=B.device)
+        slab = full[a:int(self.bounds[rank + 1])]  # this rank's C rows, ldc = N
+
+        if self._compute_rows is not None:  # injected (CPU tests): rows [lo, hi) only
+            def chunk(j, lo, hi):
+                slab[lo - a:hi - a] = self._compute_rows(self.rowptr, self.colind, vals_local, B, reduce,
+                                                         lo - a, hi - a)
+            return gather_C_overlapped(chunk, full, self.bounds, chunks, self.group)
+
+        comp = torch.cuda.current_stream(B.device)
+        if self._comm_stream is None:
+            self._comm_stream = torch.cuda.Stream(device=B.device)
+
+        def chunk(j, lo, hi):
+            self._plan.execute_rows(vals_local, B, lo - a, hi - a, out=slab, reduce=reduce,
+                                    stream=comp)
+
+        return gather_C_overlapped(chunk, full, self.bounds, chunks, self.group,
+                                   cuda_streams=(comp, self._comm_stream))

@@ -110,6 +110,23 @@ class Plan:
             1 if accumulate else 0, _stream_handle(stream, B.device)))
         return out
 
+    def execute_rows(self, vals, B, row_begin: int, row_end: int, out, reduce="sum",
+                     accumulate: bool = False, stream=None):
+        """One row chunk of execute (gespmm_plan_execute_rows): after chunks
+        [0, r1), [r1, r2), ..., [r_j, r_j+1) ran in order on one stream, C rows
+        < r_j+1 are final.  All chunks together equal execute() bit for bit."""
+        _check_csr_tensors(self.rowptr, self.colind, vals)
+        _check_dense("B", B)
+        _check_dense("out", out)
+        N = B.shape[1]
+        if B.shape[0] != self.K or tuple(out.shape) != (self.M, N):
+            raise Error(ErrorKind.InvalidArgument, "B must be K x N and out M x N")
+        _lib.check(_L.gespmm_plan_execute_rows(
+            self._h, int(row_begin), int(row_end), N, self.rowptr.data_ptr(), self.colind.data_ptr(),
+            vals.data_ptr(), B.data_ptr(), B.stride(0), out.data_ptr(), out.stride(0),
+            _reduce_code(reduce), 1 if accumulate else 0, _stream_handle(stream, B.device)))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             _L.gespmm_plan_destroy(self._h)

@@ -480,3 +480,62 @@ def test_reference_side_cpp_adapter(cuda, tmp_path):
         ref = np.asarray(g["C"], np.float64)
         scale = np.maximum(np.abs(ref), 1.0)
         assert np.all(np.abs(got - ref) <= 1e-5 * scale * 64), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("op", ["sum", "max", "mean"])
+def test_execute_rows_chunks_equal_execute(cuda, oracle_mod, op):
+    """gespmm_plan_execute_rows: consecutive row chunks on one stream equal one
+    execute bit for bit, and after chunk j every row < r_j+1 is already final
+    (the contract the overlapped all-gather relies on)."""
+    import torch
+
+    from paper_2503_08946_b200.spmm import Plan
+
+    rng = np.random.default_rng(50)
+    M, K, N = 30_000, 5_000, 64
+    long_rows = [(7_000, 2_000), (7_001, 300), (15_000, 257), (29_999, 900)]
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 10, long_rows)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, vals, B)
+    plan = Plan(rp, ci, K)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+    cuts = [0, 1, 6_999, 7_000, 7_001, 7_002, 12_345, 15_000, 29_998, M]
+    out = torch.full((M, N), float("nan"), device=cuda)
+    for j in range(len(cuts) - 1):
+        plan.execute_rows(vv, Bt, cuts[j], cuts[j + 1], out=out, reduce=op)
+        torch.cuda.synchronize()
+        done = out[:cuts[j + 1]].cpu().numpy()
+        np.testing.assert_array_equal(done, want[:cuts[j + 1]])
+    np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def test_overlapped_allgather_nccl_single_rank(cuda, oracle_mod):
+    """ShardedSpMM(chunks=4, gather=True) over NCCL (world 1 on the one GPU):
+    execute_rows on the compute stream, broadcasts on a comm stream."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_08946_b200 import sharded as S
+
+    rng = np.random.default_rng(51)
+    M, K, N = 20_000, 3_000, 64
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 10, [(5_000, 1_500)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=cuda)
+    try:
+        rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, vals, B)
+        bounds = S.partition(rowptr, 1)
+        sh = S.ShardedSpMM(rp, ci, K, bounds)
+        for op in ("sum", "min"):
+            C = sh(vv, Bt, op, gather=True, chunks=4)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(C.cpu().numpy(),
+                                          oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+    finally:
+        dist.destroy_process_group()

@@ -52,11 +52,19 @@ def _worker(rank, world, port, q):
         def twin(rp_, ci_, vv_, B_, op):
             return torch.from_numpy(O.spmm_f32(rp_, ci_, vv_, B_.numpy(), op, seg_len=256))
 
+        def twin_rows(rp_, ci_, vv_, B_, op, r0, r1):  # rows [r0, r1) of the local block only
+            p0, p1 = int(rp_[r0]), int(rp_[r1])
+            return torch.from_numpy(O.spmm_f32(rp_[r0:r1 + 1] - p0, ci_[p0:p1], vv_[p0:p1], B_.numpy(), op,
+                                               seg_len=256))
+
         sh = S.ShardedSpMM(rp, ci, B_full.shape[0], bounds, root=0, compute=twin)
+        shc = S.ShardedSpMM(rp, ci, B_full.shape[0], bounds, root=0, compute_rows=twin_rows)
         out = {}
         for op in ("sum", "max", "mean"):
             C = sh(vv, B, op, gather=True)
             out[op] = C.numpy()
+            Cc = shc(vv, B, op, gather=True, chunks=3, broadcast=False)  # overlapped all-gather
+            assert np.array_equal(Cc.numpy(), out[op]), op
         assert np.array_equal(B.numpy(), B_full)  # broadcast reached every rank
         q.put((rank, out, bounds.tolist()))
     finally:
