@@ -25,8 +25,11 @@ constexpr int kWarpsPerBlock = 8;
 // Per-warp shared-memory stage for one item's (col, val) stream.  An item holds
 // at most kTileWork + kSeg + kRowCost - 1 nonzeros (a tile) or kSeg (a segment);
 // staging starts at the 16-byte-aligned position below the item start.
-constexpr int kStageCap = 640;
-static_assert(kTileWork + kSeg + kRowCost + 2 <= kStageCap, "stage too small for the largest item");
+// 576: 8 warps x 576 x 8 B = 36.9 KB per CTA, so three CTAs fit per SM next
+// to the gather ring (8 x 4 KB); the bound below covers the 4-alignment of the
+// stage start and the rounding of its end up to a batch of 8.
+constexpr int kStageCap = 576;
+static_assert(kTileWork + kSeg + kRowCost + 2 + 3 + 8 <= kStageCap, "stage too small for the largest item");
 // Low 40 bits of the packed plan scan carry tile work, high 24 bits segment counts.
 constexpr int kPackShift = 40;
 // Column panels: B slabs larger than this are processed in column panels
@@ -49,6 +52,7 @@ struct Variant {
   int vec = 1;
   int cwm = 1;
   bool pair = false;
+  bool ring = false;  // B rows through the shared-memory cp.async ring (gespmm_kernel.cuh Ring)
 };
 
 // Everything the SpMM kernel reads.  Passed by value (kernel parameter space).

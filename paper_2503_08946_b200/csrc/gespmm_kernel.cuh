@@ -113,22 +113,31 @@ __device__ __forceinline__ void gather_off(float* d, const float* base, uint32_t
 #define GESPMM_LDNC "ld.global.nc"
 #define GESPMM_POL(n) ""
 #endif
+// GESPMM_ADDR_IMAD=1: the address is spelled mul.wide.u32 + add.s64, which
+// ptxas emits as ONE IMAD.WIDE.U32 (mad.wide.u32 by 4 becomes LEA + LEA.HI.X).
+#ifndef GESPMM_ADDR_IMAD
+#define GESPMM_ADDR_IMAD 0  // measured: IMAD.WIDE form 0.367 vs LEA pair 0.365 ms (config 2): not issue-bound
+#endif
+#if GESPMM_ADDR_IMAD
+#define GESPMM_ADDR(o, b) " .reg .u64 a, t;\n mul.wide.u32 t, %" #o ", 4;\n add.s64 a, t, %" #b ";\n "
+#else
+#define GESPMM_ADDR(o, b) " .reg .u64 a;\n mad.wide.u32 a, %" #o ", 4, %" #b ";\n "
+#endif
 template <>
 __device__ __forceinline__ void gather_off<1>(float* d, const float* base, uint32_t off, uint64_t pol) {
-  asm("{\n .reg .u64 a;\n mad.wide.u32 a, %1, 4, %2;\n " GESPMM_LDNC ".f32 %0, [a]" GESPMM_POL(3) ";\n}"
+  asm("{\n" GESPMM_ADDR(1, 2) GESPMM_LDNC ".f32 %0, [a]" GESPMM_POL(3) ";\n}"
       : "=f"(d[0])
       : "r"(off), "l"(base), "l"(pol));
 }
 template <>
 __device__ __forceinline__ void gather_off<2>(float* d, const float* base, uint32_t off, uint64_t pol) {
-  asm("{\n .reg .u64 a;\n mad.wide.u32 a, %2, 4, %3;\n " GESPMM_LDNC ".v2.f32 {%0, %1}, [a]" GESPMM_POL(4) ";\n}"
+  asm("{\n" GESPMM_ADDR(2, 3) GESPMM_LDNC ".v2.f32 {%0, %1}, [a]" GESPMM_POL(4) ";\n}"
       : "=f"(d[0]), "=f"(d[1])
       : "r"(off), "l"(base), "l"(pol));
 }
 template <>
 __device__ __forceinline__ void gather_off<4>(float* d, const float* base, uint32_t off, uint64_t pol) {
-  asm("{\n .reg .u64 a;\n mad.wide.u32 a, %4, 4, %5;\n " GESPMM_LDNC
-      ".v4.f32 {%0, %1, %2, %3}, [a]" GESPMM_POL(6) ";\n}"
+  asm("{\n" GESPMM_ADDR(4, 5) GESPMM_LDNC ".v4.f32 {%0, %1, %2, %3}, [a]" GESPMM_POL(6) ";\n}"
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
       : "r"(off), "l"(base), "l"(pol));
 }
@@ -174,6 +183,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 #endif
 }
+// 16-byte cp.async of B-row bytes at element offset `off` from `base` (L2
+// evict_last like the register gathers), bypassing L1.
+__device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint32_t off) {
+  asm volatile(
+      "{\n .reg .u64 a;\n .reg .b64 p;\n mad.wide.u32 a, %1, 4, %2;\n"
+      " createpolicy.fractional.L2::evict_last.b64 p, 1.0;\n"
+      " cp.async.cg.shared.global.L2::cache_hint [%0], [a], 16, p;\n}" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+      "r"(off), "l"(base)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
@@ -216,8 +236,26 @@ struct MinBlocks {
   static constexpr int value = CPL >= 8 ? 3 : GESPMM_MINBLOCKS;
 };
 
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::value)
+// Ring mode (RING = true; DESIGN.md 5.2 "Gather ring"): B rows are copied
+// into a per-warp shared-memory ring with 16-byte cp.async (no registers hold
+// in-flight data) and read back with one LDS per lane per row.  kDepth
+// batches of U rows are in flight per warp (~4 KB: U = 8 rows of 256 B at
+// VEC = 2, U = 4 rows of 512 B at VEC = 4).  Measured ceiling on config 2's
+// column stream (tools/gather_probe.cu): 0.248 ms at 24 warps/SM vs 0.311 ms
+// for register gathers with 8 rows in flight at 32 warps/SM.
+template <int VEC, int CWM>
+struct Ring {
+  static constexpr int kRowBytes = 128 * VEC * CWM;     // one B row, the warp's columns
+  static constexpr int kLanesPerRow = kRowBytes / 16;   // 16-byte chunks per row
+  static constexpr int kRowsPerIssue = kLanesPerRow >= 32 ? 1 : 32 / kLanesPerRow;
+  static constexpr int U = kRowBytes >= 512 ? 4 : 8;
+  static constexpr int kDepth = 2;
+  static constexpr int kWarpBytes = kDepth * U * kRowBytes;
+  static constexpr bool kSupported = CWM == 1 && VEC >= 2;  // N = 64 / 128 column tiles
+};
+
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC * CWM>::value)
     spmm_kernel(const KParams P) {
   using SR = Semiring<OP>;
   // sum/mean: two FMA chains per row (even/odd offsets from the row start),
@@ -227,7 +265,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
   // even chain).  max/min: one chain in slot 0.
   constexpr bool TWO = SR::kFma2;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
-  constexpr int U = Pipe<CPL>::U;      // gathers per batch
+  constexpr int U = RING ? Ring<VEC, CWM>::U : Pipe<CPL>::U;  // gathers per batch
+  using RG = Ring<VEC, CWM>;
+  static_assert(!RING || RG::kSupported, "ring mode: CWM == 1, VEC >= 2");
   constexpr int TW = 32 * VEC;         // columns per CWM tile
   __shared__ __align__(16) int scol[kWarpsPerBlock][kStageCap];
   __shared__ __align__(16) float sval[kWarpsPerBlock][kStageCap];
@@ -249,6 +289,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     bw[w] = P.B + woff[w];
   }
   const int64_t ldb = P.ldb;
+  // ring: this lane copies 16-byte chunk (lane % kLanesPerRow) of row
+  // (lane / kLanesPerRow) of every kRowsPerIssue-row group; a chunk past N
+  // copies column 0 (valid memory, never read back)
+  extern __shared__ float4 ring_smem[];
+  float4* const ring = ring_smem + warp * (RING ? RG::kWarpBytes / 16 : 0);
+  const int rchunk = lane % RG::kLanesPerRow;
+  const int rsub = RG::kLanesPerRow >= 32 ? 0 : lane / RG::kLanesPerRow;
+  const float* const rsrc = [&] {
+    const int64_t c = static_cast<int64_t>(cb) * TW + 4 * rchunk;
+    return P.B + (c < P.N ? c : 0);
+  }();
   int* const sc = scol[warp];
   float* const sv = sval[warp];
   int* const rp = rpw[warp];
@@ -423,6 +474,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
     else row_seed(lo, crow);
 
     // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
+    // ring: copy batch qb into slot, one commit group per batch
+    auto issue_ring = [&](int qb, int slot) {
+      float4* dst = ring + slot * (U * RG::kLanesPerRow);
+#pragma unroll
+      for (int g = 0; g < U; g += RG::kRowsPerIssue) {
+        const int u = g + rsub;
+        const uint32_t off = static_cast<uint32_t>(sc[qb - sbase + u]);
+        cp_async16_b(dst + u * RG::kLanesPerRow + rchunk, rsrc, off);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     auto issue = [&](int qb, float (&b)[U][CWM][VEC]) {
       const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
 #pragma unroll
@@ -433,6 +495,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
         gather(b[4 * g + 2], o.z);
         gather(b[4 * g + 3], o.w);
       }
+    };
+    auto ring_row = [&](int slot, int u, float (&d)[CWM][VEC]) {
+      const float* r = reinterpret_cast<const float*>(ring + (slot * U + u) * RG::kLanesPerRow);
+      Vec<VEC>::ld(d[0], r + lane * VEC);
     };
     auto consume = [&](int qb, const float (&b)[U][CWM][VEC]) {
       const float4* vp = reinterpret_cast<const float4*>(sv + (qb - sbase));
@@ -463,7 +529,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
         fold(u & 1, v[u], b[u], first_ok && p == rs);
       }
     };
-    if (lo < hi) {
+    if (RING && lo < hi) {
+      const int nb = (send - sbase) / U;
+      issue_ring(sbase, 0);
+      for (int k = 0; k < nb; ++k) {
+        if (k + 1 < nb) issue_ring(sbase + (k + 1) * U, (k + 1) & 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();  // every lane's chunks of batch k are in the ring
+        float ba[U][CWM][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ring_row(k & 1, u, ba[u]);
+        consume(sbase + k * U, ba);
+        __syncwarp();  // slot k & 1 is refilled at iteration k + 1
+      }
+    } else if (lo < hi) {
       if (Pipe<CPL>::kDouble) {
         float ba[U][CWM][VEC];
         float bb[U][CWM][VEC];
@@ -561,10 +641,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<VEC * CWM>::val
   }  // item loop
 }
 
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32>
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING>
 cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks == 0) return cudaSuccess;
+  const int smem = RING ? kWarpsPerBlock * Ring<VEC, CWM>::kWarpBytes : 0;
   // persistent grid: every resident CTA slot once (per column block)
   static thread_local int cached_dev = -1, cached_slots = 0;
   int dev = 0;
@@ -572,26 +653,34 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   if (dev != cached_dev) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32>,
-                                                  kWarpsPerBlock * 32, 0);
+    if (RING)
+      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING>,
+                                                  kWarpsPerBlock * 32, smem);
     cached_slots = sms * (per_sm > 0 ? per_sm : 1);
     cached_dev = dev;
   }
   const int64_t slots = (cached_slots + p.ncb - 1) / p.ncb;
   if (blocks > slots) blocks = slots;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(p.ncb), 1);
-  spmm_kernel<OP, VEC, CWM, OFF32><<<grid, kWarpsPerBlock * 32, 0, s>>>(p);
+  spmm_kernel<OP, VEC, CWM, OFF32, RING><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 template <gespmm_reduce_t OP, bool OFF32>
 cudaError_t launch_off(const Variant& v, const KParams& p, cudaStream_t s) {
-  if (v.vec == 4 && v.cwm == 2) return launch_t<OP, 4, 2, OFF32>(p, s);
-  if (v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, OFF32>(p, s);
-  if (v.vec == 2 && v.cwm == 2) return launch_t<OP, 2, 2, OFF32>(p, s);
-  if (v.vec == 2 && v.cwm == 1) return launch_t<OP, 2, 1, OFF32>(p, s);
-  if (v.vec == 1 && v.cwm == 2) return launch_t<OP, 1, 2, OFF32>(p, s);
-  return launch_t<OP, 1, 1, OFF32>(p, s);
+  // ring mode: 32-bit offsets, 16-byte aligned B rows, whole 16-byte chunks
+  const bool ring = v.ring && OFF32 && p.ldb % 4 == 0 && p.N % 4 == 0 &&
+                    reinterpret_cast<uintptr_t>(p.B) % 16 == 0;
+  if (ring && v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, OFF32, true>(p, s);
+  if (ring && v.vec == 2 && v.cwm == 1) return launch_t<OP, 2, 1, OFF32, true>(p, s);
+  if (v.vec == 4 && v.cwm == 2) return launch_t<OP, 4, 2, OFF32, false>(p, s);
+  if (v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, OFF32, false>(p, s);
+  if (v.vec == 2 && v.cwm == 2) return launch_t<OP, 2, 2, OFF32, false>(p, s);
+  if (v.vec == 2 && v.cwm == 1) return launch_t<OP, 2, 1, OFF32, false>(p, s);
+  if (v.vec == 1 && v.cwm == 2) return launch_t<OP, 1, 2, OFF32, false>(p, s);
+  return launch_t<OP, 1, 1, OFF32, false>(p, s);
 }
 
 template <gespmm_reduce_t OP>

@@ -1,6 +1,8 @@
 // gespmm_spmm.cu -- kernel dispatch and tile-shape selection.  The kernel
 // family itself is gespmm_kernel.cuh, instantiated per reduce op in
 // gespmm_spmm_{sum,max,min,mean}.cu.
+#include <cstdlib>
+
 #include "gespmm_internal.h"
 
 namespace gespmm {
@@ -25,16 +27,17 @@ int variant_cols(const Variant& v) { return v.pair ? 16 * v.vec : 32 * v.vec * v
 
 std::string variant_name(const Variant& v) {
   if (v.pair) return "pair_vec" + std::to_string(v.vec);
-  return "vec" + std::to_string(v.vec) + "_lpr32_cwm" + std::to_string(v.cwm);
+  return "vec" + std::to_string(v.vec) + "_lpr32_cwm" + std::to_string(v.cwm) + (v.ring ? "_ring" : "");
 }
 
 namespace {
 // in preference order for equal idle lanes / column blocks.  The paired-lane
 // kernel comes last: at N=64 the 32-lane kernel measured faster (0.362 vs
 // 0.382 ms on config 2); it wins only where 32 lanes would idle (N < 32).
-const Variant kVariants[] = {{4, 1, false}, {4, 2, false}, {2, 1, false}, {2, 2, false},
-                             {1, 1, false}, {1, 2, false}, {4, 1, true},  {2, 1, true},
-                             {1, 1, true}};
+const Variant kVariants[] = {{4, 1, false, false}, {4, 2, false, false}, {2, 1, false, false},
+                             {2, 2, false, false}, {1, 1, false, false}, {1, 2, false, false},
+                             {4, 1, true, false},  {2, 1, true, false},  {1, 1, true, false},
+                             {4, 1, false, true},  {2, 1, false, true}};
 bool two_chain(gespmm_reduce_t op) { return op == GESPMM_REDUCE_SUM || op == GESPMM_REDUCE_MEAN; }
 }  // namespace
 
@@ -60,7 +63,7 @@ Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, i
   Variant best{1, 1, false};
   int64_t best_idle = -1, best_ncb = 0;
   for (const Variant& c : kVariants) {
-    if (!aligned(c.vec) || (c.pair && !two_chain(op))) continue;
+    if (!aligned(c.vec) || (c.pair && !two_chain(op)) || c.ring) continue;
     const int64_t cols = variant_cols(c);
     const int64_t ncb = (N + cols - 1) / cols;
     const int64_t idle = ncb * cols - N;
@@ -70,6 +73,14 @@ Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, i
       best_ncb = ncb;
     }
   }
+  // the shared-memory gather ring for the 32-lane N = 64 / 128 tiles, opt-in
+  // (GESPMM_RING=1): measured slower on config 2 (0.472 vs 0.366 ms) and
+  // config 3 (3.27 vs 2.14 ms), equal on configs 4/5
+  static const bool ring_on = [] {
+    const char* e = std::getenv("GESPMM_RING");
+    return e && *e == '1';
+  }();
+  if (ring_on && !best.pair && best.cwm == 1 && best.vec >= 2) best.ring = true;
   return best;
 }
 

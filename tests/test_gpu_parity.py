@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 SEG = 256
 OPS = ["sum", "max", "min", "mean"]
 VARIANTS = ["vec1_lpr32_cwm1", "vec1_lpr32_cwm2", "vec2_lpr32_cwm1", "vec2_lpr32_cwm2",
-            "vec4_lpr32_cwm1", "vec4_lpr32_cwm2", "pair_vec1", "pair_vec2", "pair_vec4"]
+            "vec4_lpr32_cwm1", "vec4_lpr32_cwm2", "pair_vec1", "pair_vec2", "pair_vec4",
+            "vec2_lpr32_cwm1_ring", "vec4_lpr32_cwm1_ring"]
 
 
 def to_dev(cuda, *arrs):

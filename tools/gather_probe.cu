@@ -39,6 +39,96 @@ __global__ void __launch_bounds__(256) probe(const float* __restrict__ B, const 
   if (a0 == 1234.5f) sink[0] = a1;
 }
 
+// Ring variant: B rows land in a per-warp shared-memory ring with cp.async
+// (16 B per lane, a half-warp per 256-byte row), D batches of U rows in
+// flight, no registers held by in-flight data; consumed with 8-byte LDS.
+template <int U, int D>
+__global__ void __launch_bounds__(256) probe_ring(const float* __restrict__ B, const int* __restrict__ idx,
+                                                  int64_t nidx, int span, float* sink) {
+  extern __shared__ float4 sm[];
+  const int lane = threadIdx.x & 31;
+  float4* ring = sm + (threadIdx.x >> 5) * (D * U * 16);
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    const int nb = static_cast<int>((s1 - s0 + U - 1) / U);
+    auto load_idx = [&](int k) {
+      const int64_t p = s0 + static_cast<int64_t>(k) * U + lane;
+      return (k < nb && lane < U && p < s1) ? __ldg(idx + p) : 0;
+    };
+    auto issue = [&](int k, int my) {
+      if (k < nb) {
+        float4* slot = ring + (k % D) * U * 16;
+#pragma unroll
+        for (int u = 0; u < U; u += 2) {
+          const int r = __shfl_sync(0xffffffffu, my, u + (lane >> 4));
+          const float* src = B + static_cast<int64_t>(r) * 64 + (lane & 15) * 4;
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(slot + (u + (lane >> 4)) * 16 + (lane & 15)));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int nxt = load_idx(0);
+    for (int k = 0; k < D - 1; ++k) {
+      const int my = nxt;
+      nxt = load_idx(k + 1);
+      issue(k, my);
+    }
+    for (int k = 0; k < nb; ++k) {
+      const int my = nxt;
+      nxt = load_idx(k + D);
+      issue(k + D - 1, my);
+      asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+      __syncwarp();
+      const float4* slot = ring + (k % D) * U * 16;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float2 v = reinterpret_cast<const float2*>(slot + u * 16)[lane];
+        a0 += v.x;
+        a1 += v.y;
+      }
+      __syncwarp();
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  if (a0 == 1234.5f) sink[0] = a1;
+}
+
+extern "C" float gather_probe_ring(const float* B, const int* idx, int64_t nidx, int U, int D, int span,
+                                   int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = 8 * D * U * 256;
+  auto set = [&](auto k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); };
+  set(probe_ring<8, 2>); set(probe_ring<8, 3>); set(probe_ring<8, 4>); set(probe_ring<16, 2>); set(probe_ring<4, 4>);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 2; ++r) {
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    const int grid = sms * blocks_per_sm;
+    if (U == 8 && D == 2) probe_ring<8, 2><<<grid, 256, smem>>>(B, idx, nidx, span, sink);
+    else if (U == 8 && D == 3) probe_ring<8, 3><<<grid, 256, smem>>>(B, idx, nidx, span, sink);
+    else if (U == 8 && D == 4) probe_ring<8, 4><<<grid, 256, smem>>>(B, idx, nidx, span, sink);
+    else if (U == 16 && D == 2) probe_ring<16, 2><<<grid, 256, smem>>>(B, idx, nidx, span, sink);
+    else probe_ring<4, 4><<<grid, 256, smem>>>(B, idx, nidx, span, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 2 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaGetLastError() == cudaSuccess ? best : -1.f;
+}
+
 extern "C" float gather_probe(const float* B, const int* idx, int64_t nidx, int U, int span,
                               int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes) {
   int dev = 0, sms = 0;

@@ -20,9 +20,13 @@ def main():
     L.gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                ctypes.c_void_p, ctypes.c_int64]
+    L.gather_probe_ring.restype = ctypes.c_float
+    L.gather_probe_ring.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
     dev = torch.device("cuda:0")
-    csr = W.rmat_csr(20, 16 * 2**20, seed=3, device=dev)
-    B = W.dense_torch(csr.K, 64, seed=2, device=dev)
+    csr = W.rmat_csr_gpu(20, 16 * 2**20, seed=3, device=dev)
+    B = W.dense_gpu(csr.K, 64, seed=2, device=dev)
     sink = torch.zeros(4, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     nnz = csr.nnz
@@ -30,10 +34,17 @@ def main():
     streams = {"csr_order": csr.colind,
                "shuffled": csr.colind[torch.randperm(nnz, device=dev)].contiguous()}
     for name, idx in streams.items():
-        for U, bps in ((8, 8), (16, 8), (8, 4), (16, 4)):
+        for U, bps in ((8, 8), (16, 8), (8, 4), (16, 4), (8, 3)):
             ms = L.gather_probe(B.data_ptr(), idx.data_ptr(), nnz, U, 256, bps, 5, sink.data_ptr(),
                                 flush.data_ptr(), flush.numel())
             out["results"].append({"stream": name, "U": U, "warps_per_sm": 8 * bps, "ms": ms,
+                                   "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
+        if name != "csr_order":
+            continue
+        for U, D, bps in ((8, 2, 4), (8, 3, 4), (8, 4, 3), (16, 2, 3), (4, 4, 4), (8, 2, 3), (8, 3, 3)):
+            ms = L.gather_probe_ring(B.data_ptr(), idx.data_ptr(), nnz, U, D, 256, bps, 5, sink.data_ptr(),
+                                     flush.data_ptr(), flush.numel())
+            out["results"].append({"stream": name, "ring": f"U{U}xD{D}", "warps_per_sm": 8 * bps, "ms": ms,
                                    "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
     print(json.dumps(out))
 
