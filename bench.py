@@ -289,10 +289,16 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # GESPMM_BENCH_BACKEND=gloo (testing only): several ranks may share one GPU
+    backend = os.environ.get("GESPMM_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     spec = workload_spec(args.workload)
     N = spec["N"]
@@ -389,7 +395,7 @@ def main():
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:  # ncu bytes of the single-GPU launch
         try:
             with open(tpath) as f:
                 traffic = json.load(f).get(f"{args.workload}:{args.op}")

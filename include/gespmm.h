@@ -236,6 +236,19 @@ gespmm_status_t gespmm_sharded_spmm(void* comm, int world, int rank, int root,
                                     int accumulate, float* C_full, int64_t ldc_full,
                                     const int64_t* row_bounds, void* stream);
 
+/* As gespmm_sharded_spmm, with the C all-gather overlapped with the
+ * computation: each slab is computed in `chunks` row
+ * chunks (gespmm_plan_execute_rows) and chunk j of every slab is broadcast by
+ * its owner on an internal comm stream while chunk j+1 is computed.
+ * chunks = 1 is gespmm_sharded_spmm.  Returns after the gather has drained. */
+gespmm_status_t gespmm_sharded_spmm_chunked(void* comm, int world, int rank, int root,
+                                            gespmm_plan_t plan, int64_t M_local, int64_t K, int64_t N,
+                                            int64_t nnz_local, const int32_t* rowptr,
+                                            const int32_t* colind, const float* vals, float* B,
+                                            int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                            int accumulate, float* C_full, int64_t ldc_full,
+                                            const int64_t* row_bounds, int chunks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

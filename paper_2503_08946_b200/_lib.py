@@ -27,6 +27,7 @@ EXPORTS = [
     "gespmm_panel_width", "gespmm_partition_rows",
     "gespmm_rmat_csr", "gespmm_uniform_fill",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
+    "gespmm_sharded_spmm_chunked",
 ]
 
 _i64 = ctypes.c_int64
@@ -84,6 +85,9 @@ def load():
         "gespmm_sharded_spmm": ([_vp, _int, _int, _int, _vp, _i64, _i64, _i64, _i64, _vp, _vp,
                                  _vp, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64, _vp, _vp],
                                 _int),
+        "gespmm_sharded_spmm_chunked": ([_vp, _int, _int, _int, _vp, _i64, _i64, _i64, _i64, _vp, _vp,
+                                         _vp, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64, _vp, _int,
+                                         _vp], _int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

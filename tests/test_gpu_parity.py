@@ -540,3 +540,40 @@ def test_overlapped_allgather_nccl_single_rank(cuda, oracle_mod):
                                           oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_capi_sharded_spmm_single_rank(cuda, oracle_mod, chunks):
+    """gespmm_sharded_spmm[_chunked] through the C-ABI (NCCL resolved by dlopen,
+    world 1 on the one GPU): B broadcast, local slab, C all-gather (overlapped
+    with the computation when chunks > 1) -- bit-exact to the twin."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_08946_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(60)
+    M, K, N = 12_000, 2_000, 64
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 10, [(3_000, 1_200)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, vals, B)
+    uid = ctypes.create_string_buffer(128)
+    _lib.check(L.gespmm_comm_get_unique_id(uid))
+    comm = ctypes.c_void_p()
+    _lib.check(L.gespmm_comm_init(ctypes.byref(comm), 1, uid, 0))
+    try:
+        C = torch.empty((M, N), device=cuda)
+        Cf = torch.full((M, N), float("nan"), device=cuda)
+        bounds = (ctypes.c_int64 * 2)(0, M)
+        s = torch.cuda.current_stream(cuda).cuda_stream
+        _lib.check(L.gespmm_sharded_spmm_chunked(
+            comm, 1, 0, 0, None, M, K, N, int(rowptr[-1]), rp.data_ptr(), ci.data_ptr(), vv.data_ptr(),
+            Bt.data_ptr(), N, C.data_ptr(), N, 0, 0, Cf.data_ptr(), N, bounds, chunks, s))
+        torch.cuda.synchronize()
+        want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG)
+        np.testing.assert_array_equal(C.cpu().numpy(), want)
+        np.testing.assert_array_equal(Cf.cpu().numpy(), want)
+    finally:
+        L.gespmm_comm_destroy(comm)
