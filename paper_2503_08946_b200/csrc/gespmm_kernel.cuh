@@ -149,6 +149,12 @@ __device__ __forceinline__ void prefetch_off(const float* base, uint32_t off) {
   asm volatile("{\n .reg .u64 a;\n mad.wide.u32 a, %0, 4, %1;\n prefetch.global.L2::evict_last [a];\n}" ::"r"(off),
                "l"(base));
 }
+#ifndef GESPMM_FAST_VEC2
+#define GESPMM_FAST_VEC2 0  // in-row fast batch at two columns per lane (0 = off)
+#endif
+#ifndef GESPMM_FAST_VEC1
+#define GESPMM_FAST_VEC1 16  // in-row fast batch at one column per lane (0 = off)
+#endif
 #ifndef GESPMM_ITEM_PREFETCH
 #define GESPMM_ITEM_PREFETCH 0  // measured: no change (0.364 vs 0.363 ms config 2)
 #endif
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   constexpr bool TWO = SR::kFma2;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
   constexpr int U = RING ? Ring<VEC, CWM>::U : Pipe<CPL>::U;  // gathers per batch
+  constexpr int FB = RING ? 0 : CPL == 1 ? GESPMM_FAST_VEC1 : CPL == 2 ? GESPMM_FAST_VEC2 : 0;  // in-row fast batch
   using RG = Ring<VEC, CWM>;
   static_assert(!RING || RG::kSupported, "ring mode: CWM == 1, VEC >= 2");
   constexpr int TW = 32 * VEC;         // columns per CWM tile
@@ -559,6 +566,38 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       } else {
         float ba[U][CWM][VEC];
         for (int qb = sbase; qb < hi; qb += U) {
+          if constexpr (FB > 0) {
+            // FB gathers in flight while the next FB positions lie inside the
+            // current row (the bulk of long rows): FB/U times the MLP of the
+            // U-batch without changing any row's fold order.  One column per
+            // lane only: at 2 columns the extra buffer spills (measured
+            // 0.386 vs 0.366 ms on config 2); at 1 column (N = 32) it wins
+            // (config 3, N=32: 1.539 -> 1.306 ms).
+            while (qb >= lo && qb + FB <= min(hi, re)) {
+              float bf[FB > 0 ? FB : 4][CWM][VEC];
+              const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
+#pragma unroll
+              for (int g = 0; g < FB / 4; ++g) {
+                const int4 o = cp[g];
+                gather(bf[4 * g + 0], o.x);
+                gather(bf[4 * g + 1], o.y);
+                gather(bf[4 * g + 2], o.z);
+                gather(bf[4 * g + 3], o.w);
+              }
+              const float4* vp = reinterpret_cast<const float4*>(sv + (qb - sbase));
+              const bool first = first_ok && qb == rs;
+#pragma unroll
+              for (int g = 0; g < FB / 4; ++g) {
+                const float4 x = vp[g];
+                fold(0, x.x, bf[4 * g + 0], first && g == 0);
+                fold(1, x.y, bf[4 * g + 1], false);
+                fold(0, x.z, bf[4 * g + 2], false);
+                fold(1, x.w, bf[4 * g + 3], false);
+              }
+              qb += FB;
+            }
+            if (qb >= hi) break;
+          }
           issue(qb, ba);
           if (GESPMM_PREFETCH > 0 && OFF32 && qb + GESPMM_PREFETCH * U < hi) {
             const int4* cp = reinterpret_cast<const int4*>(sc + (qb + GESPMM_PREFETCH * U - sbase));
