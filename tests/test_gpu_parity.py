@@ -577,3 +577,28 @@ def test_capi_sharded_spmm_single_rank(cuda, oracle_mod, chunks):
         np.testing.assert_array_equal(Cf.cpu().numpy(), want)
     finally:
         L.gespmm_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_64bit_b_offsets(cuda, oracle_mod, op):
+    """K * ldb > 2^32: the kernel's 64-bit B-row addressing path (staged 32-bit
+    offsets would overflow).  B is a strided view (ldb ~ 7.2 M floats) into a
+    17 GB buffer; only its K x N window is written."""
+    import torch
+
+    from paper_2503_08946_b200.spmm import Plan
+
+    rng = np.random.default_rng(70)
+    M, K, N = 3_000, 600, 64
+    ldb = (2**32) // (K - 1) + 64  # (K-1) * ldb > 2^32
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 8, [(100, 700)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    big = torch.empty((K - 1) * ldb + N, dtype=torch.float32, device=cuda)
+    Bv = big.as_strided((K, N), (ldb, 1))
+    Bv.copy_(torch.from_numpy(B))
+    rp, ci, vv, _ = to_dev(cuda, rowptr, colind, vals, B[:1])
+    plan = Plan(rp, ci, K)
+    got = plan.execute(vv, Bv, op)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+    del big, Bv
