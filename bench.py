@@ -193,9 +193,18 @@ def cpu_baseline_port(csr, B, N, budget_s=2.5):
         if time.perf_counter() > t_end or runs >= 20:
             break
     gflops = 2.0 * csr.nnz * N / best / 1e9
+    # single host thread on a bounded row block (1 thread and nproc threads)
+    r1 = min(csr.M, int(np.searchsorted(rp, min(int(rp[-1]), 2_000_000))) + 1)
+    rp1 = rp[:r1 + 1]
+    p1 = int(rp1[-1])
+    t0 = time.perf_counter()
+    O.spmm_f32(rp1, ci[:p1], vv[:p1], Bh, "sum", seg_len=256, nthreads=1)
+    dt1 = time.perf_counter() - t0
     return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": nth, "kind": "port",
             "sample": f"full workload (M={csr.M}, nnz={csr.nnz}, N={N}), best of {runs} runs, "
-                      f"oracle/gespmm_oracle.c fp32 twin, OpenMP {nth} threads"}
+                      f"oracle/gespmm_oracle.c fp32 twin, OpenMP {nth} threads",
+            "single_thread": {"value": round(2.0 * p1 * N / dt1 / 1e9, 3), "unit": "GFLOP/s", "cores": 1,
+                              "sample": f"first {r1} rows ({p1} nnz) of the same matrix, one run"}}
 
 
 def run_reference(args):
