@@ -1,0 +1,58 @@
+"""bench.py's contract pieces that need no GPU: workload specs for every
+BASELINE config, the algorithmic byte model, the peak source,
+and the CPU-baseline leg on a small matrix."""
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+@pytest.mark.parametrize("name,N", [("config1", 32), ("config2", 64), ("config3-16", 16), ("config3-256", 256),
+                                    ("config4", 128), ("config5", 128)])
+def test_workload_specs(name, N):
+    spec = bench.workload_spec(name)
+    assert spec["N"] == N and spec["desc"]
+
+
+def test_unknown_workload_rejected():
+    with pytest.raises(SystemExit):
+        bench.workload_spec("config9")
+
+
+def test_algorithmic_bytes_config2():
+    M = K = 1 << 20
+    nnz, N = 16_085_882, 64
+    U, G = bench.algorithmic_bytes(M, K, N, nnz)
+    assert U == 4 * (M + 1) + 8 * nnz + 4 * K * N + 4 * M * N == 669_752_276
+    assert G == 4 * (M + 1) + 8 * nnz + 4 * nnz * N + 4 * M * N
+    assert G > U
+
+
+def test_peaks_source(tmp_path, monkeypatch):
+    peak, src = bench.peaks()
+    assert peak > 1000 and src
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps({"hbm_gbs": 6534.5}))
+    assert bench.peaks() == (6534.5, "measured (MEASURED_PEAKS.json hbm_gbs)")
+
+
+def test_traffic_file_covers_the_default_line():
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+        t = json.load(f)
+    assert t["config2:sum"] > 0
+
+
+def test_cpu_baseline_leg_small():
+    from paper_2503_08946_b200 import workloads as W
+
+    c = W.rmat_csr(12, 20_000, seed=3)
+    B = W.dense_torch(c.K, 16)
+    r = bench.cpu_baseline_port(c, B, 16, budget_s=0.2)
+    assert r["kind"] == "port" and r["cores"] >= 1 and r["value"] > 0
+    assert r["single_thread"]["cores"] == 1 and r["single_thread"]["value"] > 0
