@@ -411,6 +411,32 @@ def main():
         except Exception:
             traffic = None
 
+    # ---- live gather ceiling: the same column stream, gathers only ---------
+    # tools/gather_probe.cu replays this matrix's colind as B-row gathers at the
+    # kernel's memory-level parallelism (8 loads/warp, 32 warps/SM, 256-nonzero
+    # spans) with nothing else; its time is the floor for any kernel gathering
+    # the same rows in the same order.  N = 64 only.
+    gather_ceiling = None
+    probe = os.path.join(ROOT, "tools", "libgather_probe.so")
+    if N == 64 and world == 1 and os.path.exists(probe) and not os.environ.get("GESPMM_NO_PROBE"):
+        import ctypes
+
+        Lp = ctypes.CDLL(probe)
+        Lp.gather_probe.restype = ctypes.c_float
+        Lp.gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_int64]
+        sink = torch.zeros(4, device=dev)
+        pms = Lp.gather_probe(B.data_ptr(), colind.data_ptr(), nnz_loc, 8, 256, 4, 5, sink.data_ptr(),
+                              flush.data_ptr(), flush.numel() * 4)
+        pms16 = Lp.gather_probe(B.data_ptr(), colind.data_ptr(), nnz_loc, 16, 256, 4, 5, sink.data_ptr(),
+                                flush.data_ptr(), flush.numel() * 4)
+        if pms > 0:
+            gather_ceiling = {"probe_ms": pms, "kernel_ms": t_mean, "frac": pms / t_mean,
+                              "probe_ms_16_in_flight": pms16,
+                              "what": "gather-only replay of this colind stream, 8 loads/warp x 32 warps/SM "
+                                      "(tools/gather_probe.cu, best of 5, L2 flushed)"}
+
     # ---- e2e through the public host API (H2D + validate + plan + kernel + D2H)
     e2e = None
     if not args.no_e2e:
@@ -461,7 +487,8 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_model": f"U = 4(M+1) + 8nnz + 4KN + 4MN = {U} B per launch",
                          "peak_source": peak_src,
-                         "gather_bytes_G": G, "gather_GBs": G / (t_mean * 1e-3) / 1e9},
+                         "gather_bytes_G": G, "gather_GBs": G / (t_mean * 1e-3) / 1e9,
+                         "gather_ceiling": gather_ceiling},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
