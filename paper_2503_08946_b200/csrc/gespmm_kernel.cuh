@@ -191,13 +191,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 // 16-byte cp.async of B-row bytes at element offset `off` from `base` (L2
 // evict_last like the register gathers), bypassing L1.
-__device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint32_t off) {
+__device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint32_t off, uint64_t pol) {
   asm volatile(
-      "{\n .reg .u64 a;\n .reg .b64 p;\n mad.wide.u32 a, %1, 4, %2;\n"
-      " createpolicy.fractional.L2::evict_last.b64 p, 1.0;\n"
-      " cp.async.cg.shared.global.L2::cache_hint [%0], [a], 16, p;\n}" ::"r"(
+      "{\n .reg .u64 a;\n mad.wide.u32 a, %1, 4, %2;\n"
+      " cp.async.cg.shared.global.L2::cache_hint [%0], [a], 16, %3;\n}" ::"r"(
           static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-      "r"(off), "l"(base)
+      "r"(off), "l"(base), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -484,11 +483,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     // ring: copy batch qb into slot, one commit group per batch
     auto issue_ring = [&](int qb, int slot) {
       float4* dst = ring + slot * (U * RG::kLanesPerRow);
+      // the batch's offsets with 128-bit broadcast loads (no per-row LDS
+      // latency chain); each lane then picks the row it copies
+      int offs[U];
+      const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
+#pragma unroll
+      for (int g = 0; g < U / 4; ++g) {
+        const int4 o = cp[g];
+        offs[4 * g] = o.x, offs[4 * g + 1] = o.y, offs[4 * g + 2] = o.z, offs[4 * g + 3] = o.w;
+      }
+      const uint64_t pol = policy_evict_last();
 #pragma unroll
       for (int g = 0; g < U; g += RG::kRowsPerIssue) {
-        const int u = g + rsub;
-        const uint32_t off = static_cast<uint32_t>(sc[qb - sbase + u]);
-        cp_async16_b(dst + u * RG::kLanesPerRow + rchunk, rsrc, off);
+        int off = offs[g];
+#pragma unroll
+        for (int r = 1; r < RG::kRowsPerIssue; ++r) off = rsub == r ? offs[g + r] : off;
+        cp_async16_b(dst + (g + rsub) * RG::kLanesPerRow + rchunk, rsrc, static_cast<uint32_t>(off), pol);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };

@@ -73,14 +73,17 @@ Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, i
       best_ncb = ncb;
     }
   }
-  // the shared-memory gather ring for the 32-lane N = 64 / 128 tiles, opt-in
-  // (GESPMM_RING=1): measured slower on config 2 (0.472 vs 0.366 ms) and
-  // config 3 (3.27 vs 2.14 ms), equal on configs 4/5
-  static const bool ring_on = [] {
+  // The shared-memory gather ring (gespmm_kernel.cuh Ring): on for the
+  // 128-column tile (VEC = 4: 512-byte rows, DRAM-bound R-MAT configs 4/5,
+  // config 4: 3.09 -> 2.82 ms), off for the 64-column tile where the register
+  // pipeline wins (config 2: 0.367 vs 0.485 ms).  GESPMM_RING=0 / 1 / 2 forces
+  // off / on for VEC = 4 (default) / on for VEC >= 2.
+  static const int ring_mode = [] {
     const char* e = std::getenv("GESPMM_RING");
-    return e && *e == '1';
+    return e ? std::atoi(e) : 1;
   }();
-  if (ring_on && !best.pair && best.cwm == 1 && best.vec >= 2) best.ring = true;
+  if (!best.pair && best.cwm == 1 && ((ring_mode >= 1 && best.vec == 4) || (ring_mode == 2 && best.vec >= 2)))
+    best.ring = true;
   return best;
 }
 

@@ -106,7 +106,7 @@ def test_variant_selection_by_N():
     assert variant_name(16, reduce="mean") == "pair_vec1"
     assert variant_name(32) == "vec1_lpr32_cwm1"
     assert variant_name(64) == "vec2_lpr32_cwm1"
-    assert variant_name(128) == "vec4_lpr32_cwm1"
+    assert variant_name(128) == "vec4_lpr32_cwm1_ring"  # the shared-memory gather ring at 512-byte rows
     assert variant_name(256) == "vec4_lpr32_cwm2"
     assert variant_name(512) == "vec4_lpr32_cwm2"
     assert variant_name(33) == "pair_vec1"  # 3 blocks of 16: 15 idle columns vs 31

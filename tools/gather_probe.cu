@@ -39,6 +39,65 @@ __global__ void __launch_bounds__(256) probe(const float* __restrict__ B, const 
   if (a0 == 1234.5f) sink[0] = a1;
 }
 
+// Paired variant: half-warps gather different rows with 16-byte loads (two
+// 256-byte rows per warp instruction), U rows in flight per warp with the same
+// registers as the 8-byte-per-lane variant -- separates a per-request limit
+// from a per-byte one.
+template <int U>
+__global__ void __launch_bounds__(256) probe_pair(const float* __restrict__ B, const int* __restrict__ idx,
+                                                  int64_t nidx, int span, float* sink) {
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    for (int64_t base = s0; base < s1; base += U) {
+      const int my = (lane < U && base + lane < s1) ? __ldg(idx + base + lane) : 0;
+      float4 v[U / 2];
+#pragma unroll
+      for (int u = 0; u < U / 2; ++u) {
+        const int r = __shfl_sync(0xffffffffu, my, 2 * u + half);
+        v[u] = __ldg(reinterpret_cast<const float4*>(B + static_cast<int64_t>(r) * 64) + (lane & 15));
+      }
+#pragma unroll
+      for (int u = 0; u < U / 2; ++u) {
+        a0 += v[u].x + v[u].z;
+        a1 += v[u].y + v[u].w;
+      }
+    }
+  }
+  if (a0 == 1234.5f) sink[0] = a1;
+}
+
+extern "C" float gather_probe_pair(const float* B, const int* idx, int64_t nidx, int U, int span,
+                                   int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 2; ++r) {
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    const int grid = sms * blocks_per_sm;
+    if (U == 16) probe_pair<16><<<grid, 256>>>(B, idx, nidx, span, sink);
+    else if (U == 32) probe_pair<32><<<grid, 256>>>(B, idx, nidx, span, sink);
+    else probe_pair<8><<<grid, 256>>>(B, idx, nidx, span, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 2 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaGetLastError() == cudaSuccess ? best : -1.f;
+}
+
 // Ring variant: B rows land in a per-warp shared-memory ring with cp.async
 // (16 B per lane, a half-warp per 256-byte row), D batches of U rows in
 // flight, no registers held by in-flight data; consumed with 8-byte LDS.

@@ -24,6 +24,8 @@ def main():
     L.gather_probe_ring.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+    L.gather_probe_pair.restype = ctypes.c_float
+    L.gather_probe_pair.argtypes = L.gather_probe.argtypes
     dev = torch.device("cuda:0")
     csr = W.rmat_csr_gpu(20, 16 * 2**20, seed=3, device=dev)
     B = W.dense_gpu(csr.K, 64, seed=2, device=dev)
@@ -41,6 +43,12 @@ def main():
                                    "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
         if name != "csr_order":
             continue
+        for U, bps in ((8, 4), (16, 4), (32, 4)):  # U rows per warp, 16-byte loads by half-warps
+            ms = L.gather_probe_pair(B.data_ptr(), idx.data_ptr(), nnz, U, 256, bps, 5, sink.data_ptr(),
+                                     flush.data_ptr(), flush.numel())
+            out["results"].append({"stream": name, "pair": f"U{U}", "warps_per_sm": 8 * bps, "ms": ms,
+                                   "regs_per_lane_in_flight": U * 2,
+                                   "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
         for U, D, bps in ((8, 2, 4), (8, 3, 4), (8, 4, 3), (16, 2, 3), (4, 4, 4), (8, 2, 3), (8, 3, 3)):
             ms = L.gather_probe_ring(B.data_ptr(), idx.data_ptr(), nnz, U, D, 256, bps, 5, sink.data_ptr(),
                                      flush.data_ptr(), flush.numel())
