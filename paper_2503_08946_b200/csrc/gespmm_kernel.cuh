@@ -248,13 +248,16 @@ struct MinBlocks {
 // VEC = 2, U = 4 rows of 512 B at VEC = 4).  Measured ceiling on config 2's
 // column stream (tools/gather_probe.cu): 0.248 ms at 24 warps/SM vs 0.311 ms
 // for register gathers with 8 rows in flight at 32 warps/SM.
+#ifndef GESPMM_RING_DEPTH
+#define GESPMM_RING_DEPTH 2  // ring batches (D - 1 in flight while one is folded); 3 measured slower (2 CTAs/SM)
+#endif
 template <int VEC, int CWM>
 struct Ring {
   static constexpr int kRowBytes = 128 * VEC * CWM;     // one B row, the warp's columns
   static constexpr int kLanesPerRow = kRowBytes / 16;   // 16-byte chunks per row
   static constexpr int kRowsPerIssue = kLanesPerRow >= 32 ? 1 : 32 / kLanesPerRow;
   static constexpr int U = kRowBytes >= 512 ? 4 : 8;
-  static constexpr int kDepth = 2;
+  static constexpr int kDepth = GESPMM_RING_DEPTH;
   static constexpr int kWarpBytes = kDepth * U * kRowBytes;
   static constexpr bool kSupported = CWM == 1 && VEC >= 2;  // N = 64 / 128 column tiles
 };
@@ -547,18 +550,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       }
     };
     if (RING && lo < hi) {
+      constexpr int D = RG::kDepth;
       const int nb = (send - sbase) / U;
-      issue_ring(sbase, 0);
-      for (int k = 0; k < nb; ++k) {
-        if (k + 1 < nb) issue_ring(sbase + (k + 1) * U, (k + 1) & 1);
+#pragma unroll
+      for (int k = 0; k < D - 1; ++k) {  // prologue: D-1 batches in flight
+        if (k < nb) issue_ring(sbase + k * U, k);
         else asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      }
+      for (int k = 0; k < nb; ++k) {
+        if (k + D - 1 < nb) issue_ring(sbase + (k + D - 1) * U, (k + D - 1) % D);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
         __syncwarp();  // every lane's chunks of batch k are in the ring
         float ba[U][CWM][VEC];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ring_row(k & 1, u, ba[u]);
+        for (int u = 0; u < U; ++u) ring_row(k % D, u, ba[u]);
         consume(sbase + k * U, ba);
-        __syncwarp();  // slot k & 1 is refilled at iteration k + 1
+        __syncwarp();  // slot k % D is refilled at iteration k + 1
       }
     } else if (lo < hi) {
       if (Pipe<CPL>::kDouble) {
