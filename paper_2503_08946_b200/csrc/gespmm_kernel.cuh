@@ -22,11 +22,16 @@
 //  * Coarse-grained Warp Merging: each lane owns VEC consecutive columns in each
 //    of CWM column tiles, so one staged (col, val) pair feeds VEC*CWM FMAs and
 //    every B-row gather is one fully coalesced 32*VEC*4-byte warp access.
-//  * Gather pipeline: B-row gathers are issued in batches of U nonzeros into
-//    two register buffers; batch k+1 is in flight while batch k is folded, so
-//    ~2U rows per warp (4 KB at N=64) stay in flight.  The measured ceiling for
-//    this access pattern is ~19 TB/s from L2 (tools/gather_bw.cu); TMA gather4
-//    reaches only 3-7 TB/s for 256-byte rows, so the gathers stay in LDG.
+//  * Gather pipeline: B-row gathers are issued in batches of U = 8 nonzeros
+//    into one register buffer (16 registers at N=64; 32 warps/SM at 64
+//    registers), then folded; at one column per lane (N <= 32 tiles) runs of
+//    16 in-row positions are gathered at once.  The memory-level parallelism
+//    this buffer allows is the kernel's bound (tools/gather_probe.cu: the
+//    gather-only replay of the same stream at the same MLP takes ~81-85 % of
+//    the kernel's time).  TMA gather4 reaches only 3-7 TB/s for 256-byte rows,
+//    so the gathers stay in LDG.  At 512-byte rows (N=128 tiles) the B rows
+//    instead go through a per-warp shared-memory ring with cp.async (Ring<>),
+//    which wins where the gathers miss L2.
 //  * Rows inside a tile are reduced sequentially in ascending p.  A batch that
 //    lies inside the current row is folded check-free; a batch that crosses a
 //    row end stores finished rows (streaming stores) and steps empty rows.
@@ -210,8 +215,9 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // Batch size U (a multiple of 4: the staged (col, val) pairs of a batch are
-// read with 128-bit shared loads) and buffering: two register buffers of
-// U*VEC*CWM floats, except for 8 columns per lane (one buffer, U = 4).
+// read with 128-bit shared loads): 8 at <= 2 columns per lane, 4 at 4 or 8.
+// One register buffer of U*VEC*CWM floats (GESPMM_DOUBLE=1: two, measured
+// slower -- they spill at the 64-register cap).
 #ifndef GESPMM_U_NARROW
 #define GESPMM_U_NARROW 8  // batch for <= 2 columns per lane
 #endif
