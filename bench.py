@@ -48,6 +48,7 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config2")
     ap.add_argument("--op", default="sum", choices=["sum", "max", "min", "mean"])
+    ap.add_argument("--N", type=int, default=0, help="override the workload's dense width (sweeps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
@@ -310,6 +311,9 @@ def main():
             dist.init_process_group(backend)
 
     spec = workload_spec(args.workload)
+    if args.N > 0:
+        spec["N"] = args.N
+        spec["desc"] += f" [N overridden to {args.N}]"
     N = spec["N"]
     if args.variant:
         set_variant_override(args.variant)
