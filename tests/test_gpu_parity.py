@@ -602,3 +602,34 @@ def test_64bit_b_offsets(cuda, oracle_mod, op):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(got.cpu().numpy(), oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
     del big, Bv
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_max_nnz_near_int32_limit(cuda, oracle_mod, op):
+    """The largest nnz the int32 CSR contract admits (2^31 - 2048): 1024 rows of
+    ~2.1 M nonzeros (8,191 segments each), N=4.  Exercises every position /
+    segment / partial-slot computation at its upper range; sampled rows
+    (incl. first/last) bit-exact to the twin."""
+    import torch
+
+    from paper_2503_08946_b200 import workloads as W
+    from paper_2503_08946_b200.spmm import Plan
+
+    M, K, N = 1024, 4096, 4
+    nnz = 2**31 - 2048
+    per = nnz // M
+    rowptr = torch.arange(M + 1, dtype=torch.int64, device=cuda) * per
+    rowptr[-1] = nnz
+    rowptr = rowptr.to(torch.int32)
+    pos = torch.arange(nnz, dtype=torch.int32, device=cuda)
+    colind = (pos * 7 + (pos >> 12)) % K
+    vals = ((pos % 13) - 6).to(torch.float32) * 0.125
+    del pos
+    csr = W.Csr(rowptr, colind, vals, M, K)
+    B = W.dense_gpu(K, N, seed=4, device=cuda)
+    plan = Plan(rowptr, colind, K)
+    C = plan.execute(vals, B, op)
+    torch.cuda.synchronize()
+    sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3)
+    del csr, colind, vals, plan
+    torch.cuda.empty_cache()
