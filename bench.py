@@ -52,6 +52,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-allgather", action="store_true", help="N > 1: skip the C all-gather timing")
     ap.add_argument("--soak-s", type=float, default=1.5)
     ap.add_argument("--variant", default="", help="kernel variant override (testing), e.g. vec1_lpr32_cwm2")
     ap.add_argument("--ref-sample-products", type=int, default=800_000,
@@ -206,6 +207,65 @@ def cpu_baseline_port(csr, B, N, budget_s=2.5):
                       f"oracle/gespmm_oracle.c fp32 twin, OpenMP {nth} threads",
             "single_thread": {"value": round(2.0 * p1 * N / dt1 / 1e9, 3), "unit": "GFLOP/s", "cores": 1,
                               "sample": f"first {r1} rows ({p1} nnz) of the same matrix, one run"}}
+
+
+def time_allgather(plan, vals, B, C, bounds, rank, world, op, stream, dev, reps=5):
+    """Device time (max over ranks) of compute + C all-gather, fused vs NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_08946_b200.spmm import ipc_close, ipc_handle, ipc_open
+
+    M = int(bounds[-1])
+    a, b = int(bounds[rank]), int(bounds[rank + 1])
+    N = B.shape[1]
+    full_f = torch.empty((M, N), dtype=torch.float32, device=dev)
+    full_n = torch.empty((M, N), dtype=torch.float32, device=dev)
+    h, off = ipc_handle(full_f)
+    allh = [None] * world
+    dist.all_gather_object(allh, (h, off))
+    opened, peers = [], []
+    for w, (hw, ow) in enumerate(allh):
+        if w != rank:
+            base = ipc_open(hw)
+            opened.append(base)
+            peers.append(base + ow)
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps + 1):
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dist.barrier()  # every rank's peer stores have landed
+            ts.append(e0.elapsed_time(e1))
+        t = torch.tensor([sum(ts[1:]) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def fused():
+        plan.execute_peers(vals, B, full_f[a:b], peers, a, reduce=op, stream=stream)
+
+    def nccl():
+        plan.execute(vals, B, op, out=full_n[a:b], stream=stream)
+        for w in range(world):
+            lo, hi = int(bounds[w]), int(bounds[w + 1])
+            if hi > lo:
+                dist.broadcast(full_n[lo:hi], src=w)
+
+    t_f = timed(fused)
+    t_n = timed(nccl)
+    same = bool(torch.equal(full_f, full_n))
+    for base in opened:
+        ipc_close(base)
+    return {"fused_peer_stores_ms": t_f, "nccl_broadcasts_ms": t_n, "identical": same,
+            "bytes_per_rank": int((b - a) * N * 4 * (world - 1)),
+            "what": "compute + full C on every rank; fused = kernel epilogue stores into every "
+                    "rank's full C over NVLink (CUDA IPC), nccl = execute then one broadcast per slab owner"}
 
 
 def run_reference(args):
@@ -415,6 +475,18 @@ def main():
         except Exception:
             traffic = None
 
+    # ---- C all-gather (N > 1): fused peer stores vs NCCL after the compute --
+    # The fused path (gespmm_plan_execute_peers) writes every finished C row
+    # into every rank's full-C buffer over NVLink from the kernel epilogue
+    # (CUDA IPC); the baseline computes the slab, then one NCCL broadcast per
+    # slab owner.  Both timed on the device, max over ranks.
+    c_allgather = None
+    if world > 1 and not args.no_allgather:
+        try:
+            c_allgather = time_allgather(plan, vals, B, C, bounds, rank, world, args.op, stream, dev)
+        except Exception as ex:  # report, never fail the bench line
+            c_allgather = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+
     # ---- live gather ceiling: the same column stream, gathers only ---------
     # tools/gather_probe.cu replays this matrix's colind as B-row gathers at the
     # kernel's memory-level parallelism (8 loads/warp, 32 warps/SM, 256-nonzero
@@ -496,6 +568,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
+            "c_allgather": c_allgather,
             "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]) * n_panels,
             "panel_cols": pw,
             "kernel_variant": variant_name(N, B, C, args.op),

@@ -177,6 +177,27 @@ const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const fl
                                 int64_t ldc, gespmm_reduce_t op);
 gespmm_status_t gespmm_set_variant_override(const char* name);
 
+/* gespmm_plan_execute with a FUSED C all-gather (SURVEY.md 8 e "fusion
+ * option", f4): the kernel stores every finished C row both into C (this
+ * rank's slab, ld = ldc) and into each of peers[0..n_peers) -- full-C buffers
+ * of the node's GPUs (opened with gespmm_ipc_open_handle; P2P stores over
+ * NVLink) or this GPU's own -- at row peer_row0 + (local row), same ld.  The
+ * transfer overlaps the computation row by row; no collective call.  The
+ * caller synchronizes the ranks afterwards (stream sync + a barrier) before
+ * reading the full C.  n_peers <= 8. */
+gespmm_status_t gespmm_plan_execute_peers(gespmm_plan_t plan, int64_t N, const int32_t* rowptr,
+                                          const int32_t* colind, const float* vals, const float* B,
+                                          int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                          int accumulate, float* const* peers, int n_peers,
+                                          int64_t peer_row0, void* stream);
+/* CUDA IPC of a device buffer for the fused all-gather (64-byte handles).
+ * get: the handle of the allocation containing dev_ptr and dev_ptr's byte
+ * offset in it; open (in another process): the allocation's base -- add the
+ * offset.  close takes the base open returned. */
+gespmm_status_t gespmm_ipc_get_handle(void* dev_ptr, char handle[64], int64_t* offset);
+gespmm_status_t gespmm_ipc_open_handle(const char handle[64], void** dev_ptr);
+gespmm_status_t gespmm_ipc_close_handle(void* dev_ptr);
+
 /* Column-panel width for gespmm_plan_execute (DESIGN.md 5.2 "Panels"): -1 =
  * heuristic (panels of the widest power-of-two width whose K x width B slab
  * fits the L2 budget, only when B itself does not), 0 = never split, > 0 =

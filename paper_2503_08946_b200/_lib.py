@@ -22,7 +22,8 @@ SEGMENT_LEN = 256  # GESPMM_SEGMENT_LEN
 EXPORTS = [
     "gespmm_version", "gespmm_status_string", "gespmm_last_error", "gespmm_validate_csr",
     "gespmm_validate_csr_device", "gespmm_csr_spmm", "gespmm_csr_spmm_host",
-    "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_execute_rows", "gespmm_plan_destroy", "gespmm_plan_get_info",
+    "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_execute_rows", "gespmm_plan_destroy",
+    "gespmm_plan_execute_peers", "gespmm_ipc_get_handle", "gespmm_ipc_open_handle", "gespmm_ipc_close_handle", "gespmm_plan_get_info",
     "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_set_panel_override",
     "gespmm_panel_width", "gespmm_partition_rows",
     "gespmm_rmat_csr", "gespmm_uniform_fill",
@@ -70,6 +71,11 @@ def load():
         "gespmm_plan_execute_rows": ([_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
                                       _int, _int, _vp], _int),
         "gespmm_plan_destroy": ([_vp], _int),
+        "gespmm_plan_execute_peers": ([_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _int, _int, _vp, _int,
+                                       _i64, _vp], _int),
+        "gespmm_ipc_get_handle": ([_vp, ctypes.c_char_p, ctypes.POINTER(_i64)], _int),
+        "gespmm_ipc_open_handle": ([ctypes.c_char_p, ctypes.POINTER(_vp)], _int),
+        "gespmm_ipc_close_handle": ([_vp], _int),
         "gespmm_plan_get_info": ([_vp, ctypes.POINTER(PlanInfo)], _int),
         "gespmm_variant_name": ([_i64, _vp, _i64, _vp, _i64, _int], ctypes.c_char_p),
         "gespmm_set_variant_override": ([ctypes.c_char_p], _int),

@@ -6,6 +6,8 @@
 // Reference errors are C++ exceptions raceset::Error{ErrorKind}
 // (include/raceset/error.hpp:36-56); here they are status codes plus a
 // thread-local detail string with the same wording.
+#include <dlfcn.h>
+
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -220,7 +222,8 @@ int64_t panel_width(int64_t K, int64_t N) {
 gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* rowptr,
                               const int32_t* colind, const float* vals, const float* B, int64_t ldb,
                               float* C, int64_t ldc, gespmm_reduce_t op, int accumulate,
-                              const int64_t* range, const int* abort_flag, cudaStream_t s) {
+                              const int64_t* range, const int* abort_flag, cudaStream_t s,
+                              float* const* peers = nullptr, int n_peers = 0, int64_t peer_shift = 0) {
   gespmm_status_t st = GESPMM_OK;
   // Column panels (DESIGN.md 5.2 "Panels"): when B's row slab K x N does not
   // fit in L2, the columns are processed in panels of `pw` columns, one launch
@@ -231,7 +234,11 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
   const int64_t ldp = (N + 3) & ~int64_t(3);
   for (int64_t c0 = 0; c0 < N; c0 += pw) {
     const int64_t n = N - c0 < pw ? N - c0 : pw;
-    const Variant v = pick_variant(n, B + c0, ldb, C + c0, ldc, op);
+    Variant v = pick_variant(n, B + c0, ldb, C + c0, ldc, op);
+    if (n_peers > 0) {  // the fused-gather stores live in the 32-lane register kernel
+      v.pair = false;
+      v.ring = false;
+    }
     const int ncb = static_cast<int>((n + variant_cols(v) - 1) / variant_cols(v));
     if (ncb > 65535) return fail(GESPMM_INVALID_ARG, "invalid argument: N too large");
     st = ensure_workspace(plan, ldp, ncb, s);
@@ -259,6 +266,9 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     p.off32 = plan->K * ldb <= (int64_t(1) << 32);
     p.range = range;
     p.abort_flag = abort_flag;
+    p.n_peers = n_peers;
+    p.peer_shift = peer_shift;
+    for (int q = 0; q < n_peers; ++q) p.peers[q] = peers[q] + c0;  // this panel's columns
     cudaError_t e = launch_spmm(op, v, p, s);
     if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
   }
@@ -390,6 +400,64 @@ gespmm_status_t gespmm_plan_execute_rows(gespmm_plan_t plan, int64_t row_begin, 
   if (e != cudaSuccess) return cuda_fail(e, "row chunk range");
   return execute_range(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate,
                        plan->row_range, reinterpret_cast<const int*>(plan->row_range + 2), s);
+}
+
+gespmm_status_t gespmm_plan_execute_peers(gespmm_plan_t plan, int64_t N, const int32_t* rowptr,
+                                          const int32_t* colind, const float* vals, const float* B,
+                                          int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                          int accumulate, float* const* peers, int n_peers,
+                                          int64_t peer_row0, void* stream) {
+  if (!plan) return fail(GESPMM_INVALID_ARG, "invalid argument: plan is null");
+  gespmm_status_t st = check_shape(plan->M, plan->K, N, plan->nnz, ldb, ldc);
+  if (st != GESPMM_OK) return st;
+  if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peers) || peer_row0 < 0)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: need 0 <= n_peers <= 8 and peer_row0 >= 0");
+  for (int q = 0; q < n_peers; ++q)
+    if (!peers[q]) return fail(GESPMM_INVALID_ARG, "invalid argument: null peer buffer");
+  if (plan->n_items == 0) return GESPMM_OK;
+  return execute_range(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, nullptr, nullptr,
+                       as_stream(stream), peers, n_peers, peer_row0 * ldc);
+}
+
+gespmm_status_t gespmm_ipc_get_handle(void* dev_ptr, char handle[64], int64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(GESPMM_INVALID_ARG, "invalid argument: ipc handle");
+  // the handle names the whole allocation (e.g. a torch caching-allocator
+  // segment); the peer adds the offset of dev_ptr inside it
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<GetRange>(dlsym(h, "cuMemGetAddressRange_v2")) : nullptr;
+  }();
+  if (!get_range) return fail(GESPMM_NOT_SUPPORTED, "cuMemGetAddressRange_v2 unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  *offset = static_cast<int64_t>(reinterpret_cast<unsigned long long>(dev_ptr) - base);
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_ipc_open_handle(const char handle[64], void** dev_ptr) {
+  if (!dev_ptr || !handle) return fail(GESPMM_INVALID_ARG, "invalid argument: ipc handle");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_ipc_close_handle(void* dev_ptr) {
+  if (!dev_ptr) return GESPMM_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return GESPMM_OK;
 }
 
 gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {

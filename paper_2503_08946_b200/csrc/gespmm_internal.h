@@ -43,6 +43,8 @@ constexpr int kPackShift = 40;
 
 // Pipelined host path: at most this many row chunks per call.
 constexpr int kMaxChunks = 16;
+// Fused all-gather: at most this many destination buffers (one node's GPUs).
+constexpr int kMaxPeers = 8;
 
 // Kernel variant: VEC fp32 columns per lane per load (1, 2 or 4) and CWM column
 // tiles per warp (Coarse-grained Warp Merging); one warp covers 32*VEC*CWM
@@ -79,6 +81,12 @@ struct KParams {
   // *abort_flag is set (a failed on-device colind check of an earlier chunk).
   const int64_t* range;
   const int* abort_flag;
+  // Fused C all-gather (gespmm_plan_execute_peers): every C row is also stored
+  // at peers[q] + peer_shift + (its offset from C), q < n_peers -- peer GPUs'
+  // full-C buffers (CUDA IPC over NVLink) or this GPU's own.
+  float* peers[kMaxPeers];
+  int n_peers;
+  int64_t peer_shift;
 };
 
 // GESPMM_TRACE=1: phase timings of the host entry point and the plan build on

@@ -102,6 +102,20 @@ struct Vec<4> {
   }
 };
 
+// A finished C row segment: the local store plus, for the fused all-gather,
+// the same bytes into every peer's full C (P2P stores over NVLink, streaming).
+// A compile-time switch (PEERS): the peer loop perturbs register allocation
+// enough to cost 5-12 % when merely present, so only the fused-gather
+// instantiations carry it.
+template <int VEC, bool PEERS>
+__device__ __forceinline__ void store_c(const KParams& P, float* dst, const float* o) {
+  Vec<VEC>::stcs(dst, o);
+  if constexpr (PEERS) {
+    const int64_t off = (dst - P.C) + P.peer_shift;
+    for (int q = 0; q < P.n_peers; ++q) Vec<VEC>::stcs(P.peers[q] + off, o);
+  }
+}
+
 // One B-row gather: address = base + 4*off (one IMAD.WIDE.U32) and one
 // non-coherent vector load.  `base` already includes the lane's column offset.
 template <int VEC>
@@ -268,7 +282,7 @@ struct Ring {
   static constexpr bool kSupported = CWM == 1 && VEC >= 2;  // N = 64 / 128 column tiles
 };
 
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING>
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC * CWM>::value)
     spmm_kernel(const KParams P) {
   using SR = Semiring<OP>;
@@ -359,7 +373,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
 #pragma unroll
       for (int k = 0; k < VEC; ++k)
         o[k] = SR::finalize(value(w, k), deg, accumulate, (!SR::kSeedC0 && accumulate) ? c0[k] : 0.f);
-      Vec<VEC>::stcs(dst + (woff[w] - woff[0]), o);
+      store_c<VEC, PEERS>(P, dst + (woff[w] - woff[0]), o);
     }
   };
   const uint64_t bpol = GESPMM_BHINT ? policy_evict_last() : 0;
@@ -704,7 +718,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   }  // item loop
 }
 
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING>
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS = false>
 cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks == 0) return cudaSuccess;
@@ -717,9 +731,9 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (RING)
-      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING>,
+      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS>,
                                                   kWarpsPerBlock * 32, smem);
     cached_slots = sms * (per_sm > 0 ? per_sm : 1);
     cached_dev = dev;
@@ -727,13 +741,21 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   const int64_t slots = (cached_slots + p.ncb - 1) / p.ncb;
   if (blocks > slots) blocks = slots;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(p.ncb), 1);
-  spmm_kernel<OP, VEC, CWM, OFF32, RING><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
+  spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 template <gespmm_reduce_t OP, bool OFF32>
 cudaError_t launch_off(const Variant& v, const KParams& p, cudaStream_t s) {
   // ring mode: 32-bit offsets, 16-byte aligned B rows, whole 16-byte chunks
+  if (p.n_peers > 0) {  // fused all-gather: register-gather variants only
+    if (v.vec == 4 && v.cwm == 2) return launch_t<OP, 4, 2, OFF32, false, true>(p, s);
+    if (v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, OFF32, false, true>(p, s);
+    if (v.vec == 2 && v.cwm == 2) return launch_t<OP, 2, 2, OFF32, false, true>(p, s);
+    if (v.vec == 2 && v.cwm == 1) return launch_t<OP, 2, 1, OFF32, false, true>(p, s);
+    if (v.vec == 1 && v.cwm == 2) return launch_t<OP, 1, 2, OFF32, false, true>(p, s);
+    return launch_t<OP, 1, 1, OFF32, false, true>(p, s);
+  }
   const bool ring = v.ring && OFF32 && p.ldb % 4 == 0 && p.N % 4 == 0 &&
                     reinterpret_cast<uintptr_t>(p.B) % 16 == 0;
   if (ring && v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, OFF32, true>(p, s);

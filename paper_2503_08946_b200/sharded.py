@@ -142,12 +142,17 @@ class ShardedSpMM:
 
             self._plan = Plan(rowptr_local, colind_local, K)
 
-    def __call__(self, vals_local, B, reduce: str = "sum", gather: bool = False,
+    def __call__(self, vals_local, B, reduce: str = "sum", gather=False,
                  broadcast: bool = True, chunks: int = 1):
-        """chunks > 1 with gather=True: the C all-gather of chunk j overlaps the
-        computation of chunk j+1 (gather_C_overlapped)."""
+        """gather=True: C all-gather after the compute (one broadcast per slab
+        owner), overlapped with it when chunks > 1 (gather_C_overlapped);
+        gather="peer": FUSED into the kernel -- every C row is stored straight
+        into every rank's full-C buffer over NVLink (CUDA IPC), no collective
+        (gespmm_plan_execute_peers)."""
         if broadcast:
             broadcast_B(B, self.root, self.group)
+        if gather == "peer":
+            return self._gather_peer(vals_local, B, reduce)
         if gather and chunks > 1 and (self._plan is not None or self._compute_rows is not None):
             return self._gather_overlapped(vals_local, B, reduce, chunks)
         if self._compute is not None:
@@ -185,3 +190,38 @@ class ShardedSpMM:
 
         return gather_C_overlapped(chunk, full, self.bounds, chunks, self.group,
                                    cuda_streams=(comp, self._comm_stream))
+
+    def _gather_peer(self, vals_local, B, reduce):
+        """Fused all-gather: each rank's full-C buffer is opened by every other
+        rank (CUDA IPC handles exchanged over the process group); the kernel's
+        epilogue writes each finished row to all of them.  A barrier after the
+        local stream drains makes every peer's rows visible."""
+        import torch
+        import torch.distributed as dist
+
+        from .spmm import ipc_close, ipc_handle, ipc_open
+
+        rank = dist.get_rank(self.group)
+        world = dist.get_world_size(self.group)
+        if world > 8:
+            raise ValueError("fused all-gather: at most 8 ranks (one node)")
+        M = int(self.bounds[-1])
+        a, b = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        N = B.shape[1]
+        full = torch.empty((M, N), dtype=torch.float32, device=B.device)
+        h, off = ipc_handle(full)
+        allh = [None] * world
+        dist.all_gather_object(allh, (h, off), group=self.group)
+        opened, peers = [], []
+        for w, (hw, ow) in enumerate(allh):
+            if w != rank:  # this rank's rows reach `full` as the kernel's own output (slab)
+                base = ipc_open(hw)
+                opened.append(base)
+                peers.append(base + ow)
+        slab = full[a:b]
+        self._plan.execute_peers(vals_local, B, slab, peers, a, reduce=reduce)
+        torch.cuda.current_stream(B.device).synchronize()
+        dist.barrier(group=self.group)  # every rank's rows have landed in every buffer
+        for base in opened:
+            ipc_close(base)
+        return full

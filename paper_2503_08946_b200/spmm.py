@@ -127,6 +127,24 @@ class Plan:
             _reduce_code(reduce), 1 if accumulate else 0, _stream_handle(stream, B.device)))
         return out
 
+    def execute_peers(self, vals, B, out, peers, peer_row0: int, reduce="sum", accumulate: bool = False,
+                      stream=None):
+        """execute() with the fused C all-gather (gespmm_plan_execute_peers):
+        every C row also goes to each device pointer in `peers` (full-C
+        buffers with out's leading dimension) at row peer_row0 + local row."""
+        _check_csr_tensors(self.rowptr, self.colind, vals)
+        _check_dense("B", B)
+        _check_dense("out", out)
+        N = B.shape[1]
+        if B.shape[0] != self.K or tuple(out.shape) != (self.M, N):
+            raise Error(ErrorKind.InvalidArgument, "B must be K x N and out M x N")
+        arr = (ctypes.c_void_p * max(1, len(peers)))(*[int(p) for p in peers])
+        _lib.check(_L.gespmm_plan_execute_peers(
+            self._h, N, self.rowptr.data_ptr(), self.colind.data_ptr(), vals.data_ptr(), B.data_ptr(),
+            B.stride(0), out.data_ptr(), out.stride(0), _reduce_code(reduce), 1 if accumulate else 0, arr,
+            len(peers), int(peer_row0), _stream_handle(stream, B.device)))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             _L.gespmm_plan_destroy(self._h)
@@ -232,6 +250,26 @@ def variant_name(N: int, B=None, out=None, reduce="sum") -> str:
 
 def set_variant_override(name: str = "") -> None:
     _lib.check(_L.gespmm_set_variant_override(name.encode()))
+
+
+def ipc_handle(t) -> tuple:
+    """(64-byte CUDA IPC handle of the allocation holding tensor t, byte offset
+    of t in it) -- for the fused all-gather's peer buffers."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _lib.check(_L.gespmm_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)))
+    return bytes(h.raw), int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Maps a peer's allocation (CUDA IPC); returns its base device address."""
+    p = ctypes.c_void_p()
+    _lib.check(_L.gespmm_ipc_open_handle(handle, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(base: int) -> None:
+    _lib.check(_L.gespmm_ipc_close_handle(ctypes.c_void_p(base)))
 
 
 def panel_width(K: int, N: int) -> int:

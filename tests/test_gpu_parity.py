@@ -633,3 +633,87 @@ def test_max_nnz_near_int32_limit(cuda, oracle_mod, op):
     sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3)
     del csr, colind, vals, plan
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("N,op", [(64, "sum"), (32, "max"), (256, "mean"), (16, "sum")])
+def test_fused_peer_stores(cuda, oracle_mod, N, op):
+    """gespmm_plan_execute_peers: every row also lands in each peer buffer at
+    row peer_row0 + local row (one GPU: the peers are two other buffers);
+    N=16 sum (a paired-lane shape) and N=256 (column panels) included."""
+    import torch
+
+    from paper_2503_08946_b200.spmm import Plan
+
+    rng = np.random.default_rng(80 + N)
+    M, K = 5_000, 1_500
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 9, [(10, 1_300), (4_999, 300)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, vals, B)
+    plan = Plan(rp, ci, K)
+    C = torch.empty((M, N), device=cuda)
+    row0 = 777
+    fulls = [torch.full((M + 1_000, N), float("nan"), device=cuda) for _ in range(2)]
+    plan.execute_peers(vv, Bt, C, [f.data_ptr() for f in fulls], row0, reduce=op)
+    torch.cuda.synchronize()
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+    np.testing.assert_array_equal(C.cpu().numpy(), want)
+    for f in fulls:
+        np.testing.assert_array_equal(f[row0:row0 + M].cpu().numpy(), want)
+        assert torch.isnan(f[:row0]).all() and torch.isnan(f[row0 + M:]).all()
+
+
+def _peer_worker(rank, world, port, q):
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_08946_b200 import sharded as S
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(90)
+        M, K, N = 20_000, 3_000, 64
+        rowptr, colind, vals = powerlaw_csr(rng, M, K, 9, [(9_999, 2_000), (10_000, 500)])
+        B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+        bounds = S.partition(rowptr, world)
+        rp, ci, vv = S.local_block(rowptr, colind, vals, bounds, rank)
+        dev = torch.device("cuda", 0)
+        sh = S.ShardedSpMM(torch.as_tensor(rp, device=dev), torch.as_tensor(ci, device=dev), K, bounds)
+        Bt = torch.as_tensor(B, device=dev)
+        full = sh(torch.as_tensor(vv, device=dev), Bt, "sum", gather="peer", broadcast=False)
+        q.put((rank, full.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_allgather_two_processes(cuda, oracle_mod):
+    """ShardedSpMM(gather="peer") with two ranks on the one GPU: CUDA IPC
+    handles exchanged over the process group, each rank's kernel writes its
+    rows into both ranks' full-C buffers; both equal the twin."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    rng = np.random.default_rng(90)
+    M, K, N = 20_000, 3_000, 64
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 9, [(9_999, 2_000), (10_000, 500)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG)
+    np.testing.assert_array_equal(out[0], want)
+    np.testing.assert_array_equal(out[1], want)
