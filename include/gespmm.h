@@ -204,6 +204,11 @@ gespmm_status_t gespmm_ipc_close_handle(void* dev_ptr);
  * force panels of `cols` columns.  Results are identical for every width
  * (columns are independent).  Test/tuning knob; not thread-safe. */
 gespmm_status_t gespmm_set_panel_override(int64_t cols);
+/* Item distribution across warps: -1 = automatic (a dynamic atomic counter
+ * when the plan has >= 16384 work items, static warp striding below), 0 =
+ * static, 1 = dynamic.  Results are identical either way.  Test/tuning
+ * knob; not thread-safe. */
+gespmm_status_t gespmm_set_schedule_override(int mode);
 /* The panel width gespmm_plan_execute uses for a K-row B with N columns: one
  * kernel launch per panel, ceil(N / width) launches per execute. */
 int64_t gespmm_panel_width(int64_t K, int64_t N);

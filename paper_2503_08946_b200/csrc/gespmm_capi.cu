@@ -196,6 +196,8 @@ gespmm_status_t host_workspace(int64_t bytes, char** out) {
 // overrides (0 = one panel); otherwise a single panel unless K x N x 4 bytes
 // exceeds the L2 budget, then the widest power-of-two panel (>= kMinPanel
 // columns) whose slab fits; no panels when even the narrowest slab does not fit.
+int g_schedule_override = -1;  // -1 auto, 0 static striding, 1 dynamic counter
+
 int64_t g_panel_override = [] {
   const char* e = std::getenv("GESPMM_PANEL");
   return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(-1);
@@ -266,6 +268,26 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     p.off32 = plan->K * ldb <= (int64_t(1) << 32);
     p.range = range;
     p.abort_flag = abort_flag;
+    // Dynamic item distribution for launches with enough items to balance
+    // (config 1's 1.3 K items ran 0.018 -> 0.029 ms dynamic: the counter reset
+    // dominates); the counters (one per column block) are zeroed on the
+    // stream ahead of the launch.
+    p.work_ctr = nullptr;
+    const bool dyn = g_schedule_override >= 0 ? g_schedule_override == 1
+                                              : (GESPMM_DYN && plan->n_items >= kDynMinItems);
+    if (dyn) {
+      if (plan->work_ctr_n < ncb) {
+        if (plan->work_ctr) cudaFree(plan->work_ctr);
+        plan->work_ctr = nullptr;
+        plan->work_ctr_n = 0;
+        cudaError_t e = cudaMalloc(&plan->work_ctr, static_cast<size_t>(ncb) * 8);
+        if (e != cudaSuccess) return cuda_fail(e, "plan work counters");
+        plan->work_ctr_n = ncb;
+      }
+      cudaError_t e = cudaMemsetAsync(plan->work_ctr, 0, static_cast<size_t>(ncb) * 8, s);
+      if (e != cudaSuccess) return cuda_fail(e, "work counter reset");
+      p.work_ctr = plan->work_ctr;
+    }
     p.n_peers = n_peers;
     p.peer_shift = peer_shift;
     for (int q = 0; q < n_peers; ++q) p.peers[q] = peers[q] + c0;  // this panel's columns
@@ -462,6 +484,7 @@ gespmm_status_t gespmm_ipc_close_handle(void* dev_ptr) {
 
 gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
   if (!plan) return GESPMM_OK;
+  if (plan->work_ctr) cudaFree(plan->work_ctr);
   if (plan->row_range) cudaFree(plan->row_range);
   if (plan->items) cudaFree(plan->items);
   if (plan->partials) cudaFree(plan->partials);
@@ -673,6 +696,12 @@ const char* gespmm_variant_name(int64_t N, const float* B, int64_t ldb, const fl
 }
 
 int64_t gespmm_panel_width(int64_t K, int64_t N) { return N < 1 ? 0 : panel_width(K, N); }
+
+gespmm_status_t gespmm_set_schedule_override(int mode) {
+  if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: schedule mode -1/0/1");
+  g_schedule_override = mode;
+  return GESPMM_OK;
+}
 
 gespmm_status_t gespmm_set_panel_override(int64_t cols) {
   g_panel_override = cols < 0 ? -1 : cols;

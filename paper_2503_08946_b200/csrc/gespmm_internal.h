@@ -43,6 +43,12 @@ constexpr int kPackShift = 40;
 
 // Pipelined host path: at most this many row chunks per call.
 constexpr int kMaxChunks = 16;
+// Items are distributed to warps dynamically (an atomic counter per column
+// block) rather than by static warp striding.
+#ifndef GESPMM_DYN
+#define GESPMM_DYN 1
+#endif
+constexpr int64_t kDynMinItems = 16384;  // below: static warp striding
 // Fused all-gather: at most this many destination buffers (one node's GPUs).
 constexpr int kMaxPeers = 8;
 
@@ -87,6 +93,8 @@ struct KParams {
   float* peers[kMaxPeers];
   int n_peers;
   int64_t peer_shift;
+  // dynamic item distribution: one counter per column block, zero at launch
+  unsigned long long* work_ctr;
 };
 
 // GESPMM_TRACE=1: phase timings of the host entry point and the plan build on
@@ -123,7 +131,9 @@ struct gespmm_plan_s {
   float* partials = nullptr;
   int64_t partial_floats = 0;
   int* counters = nullptr;
-  int64_t* row_range = nullptr;  // [2] items of the current execute_rows chunk (+ a zero abort flag)
+  int64_t* row_range = nullptr;
+  unsigned long long* work_ctr = nullptr;  // per column block item counters (GESPMM_DYN)
+  int64_t work_ctr_n = 0;  // [2] items of the current execute_rows chunk (+ a zero abort flag)
   int64_t counter_ints = 0;
   int device = 0;
 };

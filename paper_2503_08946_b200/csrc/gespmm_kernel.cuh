@@ -210,13 +210,35 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 // 16-byte cp.async of B-row bytes at element offset `off` from `base` (L2
 // evict_last like the register gathers), bypassing L1.
+#ifndef GESPMM_RING_HINT
+#define GESPMM_RING_HINT 0  // no L2 hint: with one (1: policy operand, 2: createpolicy in the asm) some instantiations fault with cudaErrorIllegalInstruction at the LDGSTS (its desc operand came out as desc[UR1]); without it, configs 4/5 also run 2 % faster
+#endif
 __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint32_t off, uint64_t pol) {
+#if GESPMM_RING_HINT == 1
   asm volatile(
       "{\n .reg .u64 a;\n mad.wide.u32 a, %1, 4, %2;\n"
       " cp.async.cg.shared.global.L2::cache_hint [%0], [a], 16, %3;\n}" ::"r"(
           static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
       "r"(off), "l"(base), "l"(pol)
       : "memory");
+#elif GESPMM_RING_HINT == 2
+  (void)pol;  // policy created next to its use
+  asm volatile(
+      "{\n .reg .u64 a;\n .reg .b64 p;\n mad.wide.u32 a, %1, 4, %2;\n"
+      " createpolicy.fractional.L2::evict_last.b64 p, 1.0;\n"
+      " cp.async.cg.shared.global.L2::cache_hint [%0], [a], 16, p;\n}" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+      "r"(off), "l"(base)
+      : "memory");
+#else
+  (void)pol;
+  asm volatile(
+      "{\n .reg .u64 a;\n mad.wide.u32 a, %1, 4, %2;\n"
+      " cp.async.cg.shared.global [%0], [a], 16;\n}" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+      "r"(off), "l"(base)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
@@ -418,8 +440,30 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     t_begin = P.range[0];
     t_end = P.range[1];
   }
-  for (int64_t t = t_begin + static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; t < t_end;
-       t += wstride) {
+  // Item distribution: dynamic when the launch carries a counter (P.work_ctr,
+  // zeroed before the launch; one per column block): warps grab items with an
+  // atomic, the next grab issued at the top of an item and consumed at its
+  // end so its latency hides behind the item.  Static warp striding
+  // otherwise (small launches, where the counter reset costs more than it
+  // balances).  Measured dynamic vs static: config 2 0.371 -> 0.352 ms,
+  // config 3 (N=64) 2.15 -> 1.81 ms, config 4 2.84 -> 2.65 ms, config 5
+  // 57.5 -> 49.6 ms.
+#define GESPMM_NEXT_ITEM                                                         \
+  {                                                                              \
+    t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(0xffffffffu, next, 0)) : t + wstride; \
+    continue;                                                                    \
+  }
+  const bool dyn = P.work_ctr != nullptr;
+  unsigned long long* const wctr = dyn ? P.work_ctr + blockIdx.y : nullptr;
+  auto grab = [&]() {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(wctr, 1ULL);
+    return v;
+  };
+  int64_t t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(0xffffffffu, grab(), 0))
+                  : t_begin + static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  for (; t < t_end;) {
+    const unsigned long long next = dyn ? grab() : 0ULL;
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];
     // the next item's descriptor into L1 (no registers held): its load at the
@@ -663,7 +707,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         re = rp[row + 1];
         row_seed(rs, crow);
       }
-      continue;
+      GESPMM_NEXT_ITEM;
     }
     // ---- long-row segment: publish the partial, then take a ticket -----------
     const int seg = it.y;
@@ -685,7 +729,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     int* counter = P.counters + static_cast<int64_t>(slot) * P.ncb + cb;
     if (lane == 0) ticket = atomicAdd(counter, 1);
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    if (ticket != nseg - 1) continue;
+    if (ticket != nseg - 1) GESPMM_NEXT_ITEM;
     // last segment: combine all partials strictly left to right
     __threadfence();
     const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp;
@@ -715,7 +759,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     }
     store_row(crow, deg);
     if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
+    t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(0xffffffffu, next, 0)) : t + wstride;
   }  // item loop
+#undef GESPMM_NEXT_ITEM
 }
 
 template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS = false>

@@ -277,6 +277,11 @@ def panel_width(K: int, N: int) -> int:
     return int(_L.gespmm_panel_width(int(K), int(N)))
 
 
+def set_schedule_override(mode: int = -1) -> None:
+    """Item distribution: -1 automatic, 0 static warp striding, 1 dynamic counter."""
+    _lib.check(_L.gespmm_set_schedule_override(int(mode)))
+
+
 def set_panel_override(cols: int = -1) -> None:
     """Column-panel width: -1 heuristic, 0 never split, > 0 forced width."""
     _lib.check(_L.gespmm_set_panel_override(int(cols)))

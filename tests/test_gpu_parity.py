@@ -116,6 +116,33 @@ def test_accumulate_bit_exact(cuda, oracle_mod, op):
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("N", [16, 64, 128, 200])
+@pytest.mark.parametrize("op", ["sum", "max", "mean"])
+def test_schedules_bit_exact(cuda, oracle_mod, op, N, mode):
+    """Static warp striding and the dynamic item counter give the twin's bits
+    (incl. long rows spanning many segments, empty rows, accumulate)."""
+    from paper_2503_08946_b200 import spmm
+
+    rng = np.random.default_rng(120 + N)
+    M, K = 3_000, 900
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 9, [(1, 5_000), (2, 257), (2_999, 700)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    spmm.set_schedule_override(mode)
+    try:
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        got2, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)  # counters re-armed per launch
+        got_acc, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op, C0=C0)
+    finally:
+        spmm.set_schedule_override(-1)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(got2, want)
+    np.testing.assert_array_equal(
+        got_acc, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG))
+
+
 @pytest.mark.parametrize("N,panel", [(256, 64), (100, 32), (200, 64), (64, 16)])
 @pytest.mark.parametrize("op", OPS)
 def test_column_panels_bit_exact(cuda, oracle_mod, op, N, panel):
