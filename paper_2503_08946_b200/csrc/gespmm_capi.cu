@@ -273,8 +273,10 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     // dominates); the counters (one per column block) are zeroed on the
     // stream ahead of the launch.
     p.work_ctr = nullptr;
+    // (item-range launches -- row chunks of the pipelined host path and of
+    // execute_rows -- are a few thousand items each: static)
     const bool dyn = g_schedule_override >= 0 ? g_schedule_override == 1
-                                              : (GESPMM_DYN && plan->n_items >= kDynMinItems);
+                                              : (GESPMM_DYN && !range && plan->n_items >= kDynMinItems);
     if (dyn) {
       if (plan->work_ctr_n < ncb) {
         if (plan->work_ctr) cudaFree(plan->work_ctr);

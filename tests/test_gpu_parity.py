@@ -510,8 +510,9 @@ def test_reference_side_cpp_adapter(cuda, tmp_path):
         assert np.all(np.abs(got - ref) <= 1e-5 * scale * 64), np.abs(got - ref).max()
 
 
+@pytest.mark.parametrize("mode", [-1, 1])
 @pytest.mark.parametrize("op", ["sum", "max", "mean"])
-def test_execute_rows_chunks_equal_execute(cuda, oracle_mod, op):
+def test_execute_rows_chunks_equal_execute(cuda, oracle_mod, op, mode):
     """gespmm_plan_execute_rows: consecutive row chunks on one stream equal one
     execute bit for bit, and after chunk j every row < r_j+1 is already final
     (the contract the overlapped all-gather relies on)."""
@@ -529,11 +530,17 @@ def test_execute_rows_chunks_equal_execute(cuda, oracle_mod, op):
     want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
     cuts = [0, 1, 6_999, 7_000, 7_001, 7_002, 12_345, 15_000, 29_998, M]
     out = torch.full((M, N), float("nan"), device=cuda)
-    for j in range(len(cuts) - 1):
-        plan.execute_rows(vv, Bt, cuts[j], cuts[j + 1], out=out, reduce=op)
-        torch.cuda.synchronize()
-        done = out[:cuts[j + 1]].cpu().numpy()
-        np.testing.assert_array_equal(done, want[:cuts[j + 1]])
+    from paper_2503_08946_b200 import spmm
+
+    spmm.set_schedule_override(mode)  # 1: the dynamic item counter inside row ranges too
+    try:
+        for j in range(len(cuts) - 1):
+            plan.execute_rows(vv, Bt, cuts[j], cuts[j + 1], out=out, reduce=op)
+            torch.cuda.synchronize()
+            done = out[:cuts[j + 1]].cpu().numpy()
+            np.testing.assert_array_equal(done, want[:cuts[j + 1]])
+    finally:
+        spmm.set_schedule_override(-1)
     np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
