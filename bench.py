@@ -53,7 +53,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-allgather", action="store_true", help="N > 1: skip the C all-gather timing")
-    ap.add_argument("--soak-s", type=float, default=1.5)
+    ap.add_argument("--soak-s", type=float, default=0.0, help="back-to-back launches before the timed steps")
+    ap.add_argument("--sustained-s", type=float, default=1.0,
+                    help="soak length of the extra 'sustained' leg (0 = skip)")
     ap.add_argument("--variant", default="", help="kernel variant override (testing), e.g. vec1_lpr32_cwm2")
     ap.add_argument("--ref-sample-products", type=int, default=800_000,
                     help="--impl reference: nnz*N products per step (bounds interpreter RAM)")
@@ -168,7 +170,62 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "window": "soak + timed region"}
+                "samples": len(sm), "window": "nvidia-smi -lms 100"}
+
+
+class NvmlSampler:
+    """SM clock / throttle reasons polled in-process (NVML, the library
+    nvidia-smi reads) every ~2 ms while running, so a timed region of a few
+    tens of milliseconds gets its own samples without a pre-soak."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, enabled: bool = True):
+        import threading
+
+        self.ok = False
+        self.sm, self.reasons, self.mx = [], set(), 0.0
+        if not enabled:
+            return
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:
+            return
+        self.stop_evt = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_evt.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.ok:
+            self.th.start()
+
+    def stop(self, window: str):
+        if not self.ok:
+            return None
+        self.stop_evt.set()
+        self.th.join(timeout=2)
+        if not self.sm:
+            return None
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "window": window, "source": "NVML, ~2 ms"}
 
 
 def cpu_baseline_port(csr, B, N, budget_s=2.5):
@@ -429,28 +486,54 @@ def main():
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local, enabled=not args.no_clocks and rank == 0)
-    # soak: back-to-back launches so the clock samples see the kernel under load
-    t_soak = time.perf_counter() + (args.soak_s if clocks.proc is not None else 0.0)
-    while time.perf_counter() < t_soak:
-        for _ in range(50):
-            run_once()
-        torch.cuda.synchronize()
+    nvml = NvmlSampler(local, enabled=not args.no_clocks and rank == 0)
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        starts[i].record(stream)
-        run_once()
-        ends[i].record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    def soak(seconds):  # back-to-back launches (sustained load)
+        t_end_soak = time.perf_counter() + seconds
+        while time.perf_counter() < t_end_soak:
+            for _ in range(50):
+                run_once()
+            torch.cuda.synchronize()
+
+    def timed_steps():
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[i].record(stream)
+            run_once()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+
+    soak(args.soak_s)
+    nvml.start()
+    times = timed_steps()
+    clk_nvml = nvml.stop("timed region")
+    # sustained: the same steps after ~1 s of back-to-back launches (the part
+    # reaches its power cap; clocks sampled over soak + steps)
+    sustained = None
+    if args.sustained_s > 0:
+        nvml2 = NvmlSampler(local, enabled=not args.no_clocks and rank == 0)
+        nvml2.start()
+        soak(args.sustained_s)
+        times2 = timed_steps()
+        t2 = torch.tensor([sum(times2) / len(times2)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        sustained = {"ms_per_step": float(t2.item()), "soak_s": args.sustained_s,
+                     "clocks": nvml2.stop(f"{args.sustained_s} s soak + timed steps")}
     clk = clocks.stop()
+    if clk is not None:
+        clk["window"] = "whole measurement (timed region + sustained leg), nvidia-smi -lms 100"
+    if clk_nvml is not None:
+        clk_nvml["nvidia_smi"] = clk
+        clk = clk_nvml
     t_mean = sum(times) / len(times)
     t_max = torch.tensor([t_mean], device=dev, dtype=torch.float64)
     if world > 1:
@@ -568,6 +651,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
+            "sustained": sustained,
             "c_allgather": c_allgather,
             "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]) * n_panels,
             "panel_cols": pw,

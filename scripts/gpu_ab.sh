@@ -4,6 +4,6 @@ timeout 1200 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovid
 for w in "$@"; do
 for lib in paper_2503_08946_b200/libgespmm*.so; do
   b=$(basename $lib .so)
-  GESPMM_LIB=$PWD/$lib timeout 300 python bench.py --workload $w --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-clocks --soak-s 0 > gpurun_out/ab_${w}_${b}.log 2>&1
+  GESPMM_LIB=$PWD/$lib timeout 300 python bench.py --workload $w --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-clocks --soak-s 0 --sustained-s 0 > gpurun_out/ab_${w}_${b}.log 2>&1
 done
 done
