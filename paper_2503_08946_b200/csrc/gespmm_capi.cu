@@ -516,13 +516,28 @@ gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
   g_last_error.clear();
   gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
   if (st != GESPMM_OK) return st;
-  gespmm_plan_t plan = nullptr;
-  st = gespmm_plan_create(&plan, M, K, nnz, rowptr, colind, /*validate colind*/ 1, stream);
+  if (M > 0 && !rowptr) return fail(GESPMM_INVALID_ARG, "invalid argument: rowptr is null");
+  // A per-device plan object re-planned in place (no cudaMalloc/cudaFree per
+  // call: cudaFree synchronizes the device); the call returns after its
+  // launches drain, so the next call may reuse the plan's buffers.
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  static gespmm_plan_s* plans[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  gespmm_plan_s*& plan = plans[dev & 63];
+  if (!plan) {
+    plan = new gespmm_plan_s();
+    plan->device = dev;
+  }
+  plan->M = M;
+  plan->K = K;
+  plan->nnz = nnz;
+  st = build_plan(plan, rowptr, colind, /*validate colind*/ true, as_stream(stream));
   if (st != GESPMM_OK) return st;
   st = gespmm_plan_execute(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, stream);
-  // plan memory is released once the launch has drained
-  cudaStreamSynchronize(as_stream(stream));
-  gespmm_plan_destroy(plan);
+  const cudaError_t e = cudaStreamSynchronize(as_stream(stream));
+  if (st == GESPMM_OK && e != cudaSuccess) return cuda_fail(e, "spmm");
   return st;
 }
 
