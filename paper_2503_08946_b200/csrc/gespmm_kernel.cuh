@@ -132,16 +132,9 @@ __device__ __forceinline__ void gather_off(float* d, const float* base, uint32_t
 #define GESPMM_LDNC "ld.global.nc"
 #define GESPMM_POL(n) ""
 #endif
-// GESPMM_ADDR_IMAD=1: the address is spelled mul.wide.u32 + add.s64, which
-// ptxas emits as ONE IMAD.WIDE.U32 (mad.wide.u32 by 4 becomes LEA + LEA.HI.X).
-#ifndef GESPMM_ADDR_IMAD
-#define GESPMM_ADDR_IMAD 0  // measured: IMAD.WIDE form 0.367 vs LEA pair 0.365 ms (config 2): not issue-bound
-#endif
-#if GESPMM_ADDR_IMAD
-#define GESPMM_ADDR(o, b) " .reg .u64 a, t;\n mul.wide.u32 t, %" #o ", 4;\n add.s64 a, t, %" #b ";\n "
-#else
+// address = base + 4 * off in one mad.wide.u32 (ptxas: LEA + LEA.HI.X; the
+// single-IMAD.WIDE spelling measured no faster -- DESIGN.md 8.1)
 #define GESPMM_ADDR(o, b) " .reg .u64 a;\n mad.wide.u32 a, %" #o ", 4, %" #b ";\n "
-#endif
 template <>
 __device__ __forceinline__ void gather_off<1>(float* d, const float* base, uint32_t off, uint64_t pol) {
   asm("{\n" GESPMM_ADDR(1, 2) GESPMM_LDNC ".f32 %0, [a]" GESPMM_POL(3) ";\n}"
@@ -160,26 +153,12 @@ __device__ __forceinline__ void gather_off<4>(float* d, const float* base, uint3
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
       : "r"(off), "l"(base), "l"(pol));
 }
-// L2 prefetch of one B row (GESPMM_PREFETCH: distance in batches, 0 = off).
-#ifndef GESPMM_PREFETCH
-#define GESPMM_PREFETCH 0
-#endif
-__device__ __forceinline__ void prefetch_off(const float* base, uint32_t off) {
-  asm volatile("{\n .reg .u64 a;\n mad.wide.u32 a, %0, 4, %1;\n prefetch.global.L2::evict_last [a];\n}" ::"r"(off),
-               "l"(base));
-}
 #ifndef GESPMM_FAST_VEC2
 #define GESPMM_FAST_VEC2 0  // in-row fast batch at two columns per lane (0 = off)
 #endif
 #ifndef GESPMM_FAST_VEC1
 #define GESPMM_FAST_VEC1 16  // in-row fast batch at one column per lane (0 = off)
 #endif
-#ifndef GESPMM_ITEM_PREFETCH
-#define GESPMM_ITEM_PREFETCH 0  // measured: no change (0.364 vs 0.363 ms config 2)
-#endif
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -252,8 +231,8 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 // Batch size U (a multiple of 4: the staged (col, val) pairs of a batch are
 // read with 128-bit shared loads): 8 at <= 2 columns per lane, 4 at 4 or 8.
-// One register buffer of U*VEC*CWM floats (GESPMM_DOUBLE=1: two, measured
-// slower -- they spill at the 64-register cap).
+// One register buffer of U*VEC*CWM floats (two measured slower: they spill at
+// the 64-register cap).
 #ifndef GESPMM_U_NARROW
 #define GESPMM_U_NARROW 8  // batch for <= 2 columns per lane
 #endif
@@ -263,13 +242,9 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #ifndef GESPMM_ABL_NOGATHER
 #define GESPMM_ABL_NOGATHER 0
 #endif
-#ifndef GESPMM_DOUBLE
-#define GESPMM_DOUBLE 0  // measured: one buffer (60 regs, 32 warps/SM) beats two (spills)
-#endif
 template <int CPL>
 struct Pipe {
   static constexpr int U = CPL >= 4 ? 4 : GESPMM_U_NARROW;
-  static constexpr bool kDouble = GESPMM_DOUBLE && CPL <= 4;
 };
 
 #ifndef GESPMM_MINBLOCKS
@@ -466,9 +441,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     const unsigned long long next = dyn ? grab() : 0ULL;
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];
-    // the next item's descriptor into L1 (no registers held): its load at the
-    // top of the next iteration then skips a full global-memory latency
-    if (GESPMM_ITEM_PREFETCH && lane == 0 && t + wstride < t_end) prefetch_l1(P.items + t + wstride);
     const bool is_tile = it.y < 0;
     // ---- item decode: nonzero span [lo, hi) and its rows --------------------
     // A segment is run as a one-row tile whose row ends at the segment end.
@@ -633,19 +605,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         __syncwarp();  // slot k % D is refilled at iteration k + 1
       }
     } else if (lo < hi) {
-      if (Pipe<CPL>::kDouble) {
-        float ba[U][CWM][VEC];
-        float bb[U][CWM][VEC];
-        issue(sbase, ba);
-        for (int qb = sbase;; qb += 2 * U) {
-          if (qb + U < hi) issue(qb + U, bb);
-          consume(qb, ba);
-          if (qb + U >= hi) break;
-          if (qb + 2 * U < hi) issue(qb + 2 * U, ba);
-          consume(qb + U, bb);
-          if (qb + 2 * U >= hi) break;
-        }
-      } else {
+      {
         float ba[U][CWM][VEC];
         for (int qb = sbase; qb < hi; qb += U) {
           if constexpr (FB > 0) {
@@ -681,17 +641,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
             if (qb >= hi) break;
           }
           issue(qb, ba);
-          if (GESPMM_PREFETCH > 0 && OFF32 && qb + GESPMM_PREFETCH * U < hi) {
-            const int4* cp = reinterpret_cast<const int4*>(sc + (qb + GESPMM_PREFETCH * U - sbase));
-#pragma unroll
-            for (int g = 0; g < U / 4; ++g) {
-              const int4 o = cp[g];
-              prefetch_off(bw[0], o.x);
-              prefetch_off(bw[0], o.y);
-              prefetch_off(bw[0], o.z);
-              prefetch_off(bw[0], o.w);
-            }
-          }
           consume(qb, ba);
         }
       }
