@@ -190,6 +190,26 @@ extern "C" float gather_probe_ring(const float* B, const int* idx, int64_t nidx,
 
 extern "C" float gather_probe(const float* B, const int* idx, int64_t nidx, int U, int span,
                               int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes) {
+  if (reps == 0) {  // one timed run, no warm-up (the caller prepared the cache state)
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    const int grid = sms * blocks_per_sm;
+    if (U == 8) probe<8><<<grid, 256>>>(B, idx, nidx, span, sink);
+    else if (U == 16) probe<16><<<grid, 256>>>(B, idx, nidx, span, sink);
+    else probe<4><<<grid, 256>>>(B, idx, nidx, span, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return cudaGetLastError() == cudaSuccess ? ms : -1.f;
+  }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
