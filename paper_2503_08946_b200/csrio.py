@@ -158,7 +158,7 @@ def cached_csr(path: str, make, device=None):
         return Csr(np.asarray(rp), np.asarray(ci), np.asarray(vv), M, K)
     import torch
 
-    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+    t = lambda a: torch.from_numpy(np.array(a)).to(device)  # noqa: E731  (copy: memmaps are read-only)
     return Csr(t(rp), t(ci), t(vv), M, K)
 
 

@@ -122,3 +122,55 @@ def test_inst_writer_round_trip_on_generated_instance():
 def test_inst_writer_round_trips_reference_fixtures(name):
     inst = I.load_instance_file(os.path.join(REF_FIXTURES, name))
     assert I.parse_instance(csrio.format_instance(inst)) == inst
+
+
+@pytest.mark.gpu
+def test_files_to_gpu_path(tmp_path, oracle_mod):
+    """A Matrix Market file and a binary cache feed the GPU path directly; the
+    cache round trip lands on the device (cached_csr(device=...))."""
+    import torch
+
+    from paper_2503_08946_b200 import workloads as W
+    from paper_2503_08946_b200.spmm import Plan
+
+    rp, ci, vv, M, K = _csr(7, M=2000, K=700)
+    B = np.random.default_rng(1).uniform(-1, 1, (K, 48)).astype(np.float32)
+    mtx = str(tmp_path / "a.mtx")
+    csrio.write_matrix_market(mtx, rp, ci, vv, M, K)
+    r2, c2, v2, M2, K2 = csrio.read_matrix_market(mtx)
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    got = Plan(t(r2), t(c2), K2).execute(t(v2), t(B), "max")
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle_mod.spmm_f32(rp, ci, vv, B, "max", seg_len=256))
+    cache = str(tmp_path / "a.csr")
+    c = csrio.cached_csr(cache, lambda: W.Csr(rp, ci, vv, M, K), device=dev)
+    got = Plan(c.rowptr, c.colind, c.K).execute(c.vals, t(B), "sum")
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle_mod.spmm_f32(rp, ci, vv, B, "sum", seg_len=256))
+
+
+@pytest.mark.gpu
+def test_device_validation_matches_host_messages():
+    """gespmm_validate_csr_device reports the reference's messages like the host check."""
+    import torch
+
+    from paper_2503_08946_b200 import _lib
+    from paper_2503_08946_b200.errors import Error, ErrorKind
+
+    L = _lib.load()
+    dev = torch.device("cuda:0")
+    cases = [
+        (np.array([1, 2], np.int32), np.array([0, 1], np.int32), "rowPtr[0] must be 0"),
+        (np.array([0, 2, 1], np.int32), np.array([0, 1], np.int32), "nondecreasing"),
+        (np.array([0, 1, 3], np.int32), np.array([0, 1], np.int32), "rowPtr end differs"),
+        (np.array([0, 1, 2], np.int32), np.array([0, 9], np.int32), "colInd entry out of [0,5)"),
+    ]
+    for rp, ci, msg in cases:
+        M = len(rp) - 1
+        trp, tci = torch.as_tensor(rp, device=dev), torch.as_tensor(ci, device=dev)
+        st = L.gespmm_validate_csr_device(M, 5, len(ci), trp.data_ptr(), tci.data_ptr(), None)
+        with pytest.raises(Error) as ei:
+            _lib.check(st)
+        assert ei.value.kind == ErrorKind.CsrInvalid and msg in str(ei.value), (msg, str(ei.value))
+    good_rp = torch.as_tensor(np.array([0, 1, 2], np.int32), device=dev)
+    good_ci = torch.as_tensor(np.array([0, 4], np.int32), device=dev)
+    assert L.gespmm_validate_csr_device(2, 5, 2, good_rp.data_ptr(), good_ci.data_ptr(), None) == 0
