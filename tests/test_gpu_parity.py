@@ -751,3 +751,45 @@ def test_fused_peer_allgather_two_processes(cuda, oracle_mod):
     want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG)
     np.testing.assert_array_equal(out[0], want)
     np.testing.assert_array_equal(out[1], want)
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_execute_under_cuda_graph_capture(cuda, oracle_mod, op):
+    """plan.execute is capturable into a CUDA graph (after one warm-up call
+    sized the workspace): replays with new vals/B contents in the same buffers
+    give the twin's bits -- launch-bound small SpMMs (config 1) replay without
+    per-call host overhead."""
+    import torch
+
+    from paper_2503_08946_b200 import spmm
+    from paper_2503_08946_b200.spmm import Plan
+
+    rng = np.random.default_rng(140)
+    M, K, N = 4096, 4096, 32
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 20, [(17, 900)])
+    rp, ci = to_dev(cuda, rowptr, colind)
+    vv = torch.empty(colind.size, dtype=torch.float32, device=cuda)
+    Bt = torch.empty((K, N), dtype=torch.float32, device=cuda)
+    C = torch.empty((M, N), dtype=torch.float32, device=cuda)
+    plan = Plan(rp, ci, K)
+    for mode in (-1, 1):  # static striding (small plan) and the dynamic counter (memset node)
+        spmm.set_schedule_override(mode)
+        try:
+            s = torch.cuda.Stream(device=cuda)
+            with torch.cuda.stream(s):
+                plan.execute(vv, Bt, op, out=C, stream=s)  # warm-up: workspace, attributes
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                plan.execute(vv, Bt, op, out=C, stream=s)
+            for rep in range(3):
+                v = rng.uniform(-1, 1, colind.size).astype(np.float32)
+                B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+                vv.copy_(torch.from_numpy(v))
+                Bt.copy_(torch.from_numpy(B))
+                g.replay()
+                torch.cuda.synchronize()
+                np.testing.assert_array_equal(C.cpu().numpy(),
+                                              oracle_mod.spmm_f32(rowptr, colind, v, B, op, seg_len=SEG))
+        finally:
+            spmm.set_schedule_override(-1)
