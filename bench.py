@@ -9,16 +9,21 @@ requested (Graph500 a/b/c = .57/.19/.19, deduplicated), x dense B with N=64,
 fp32, sum-reduce.  Synthetic data, seeded; generated on the GPU.
 
 A step = one execution of the hot path over the matrix with a cached plan
-(one kernel launch).  Each timed step is bracketed by CUDA events on the
+(one kernel launch per column panel, after a reset of its item counter).  Each timed step is bracketed by CUDA events on the
 launching stream, with a 2x-L2 buffer written between steps (L2 flushed; the
 flush is outside the events).  N>1 (torchrun): row-block sharding, each rank
 runs its nnz-balanced row block after a one-time NCCL broadcast of B; time =
 max over ranks; value = total flops / that time ("strong" scaling).
 
-Extra keys: roofline (HBM, algorithmic compulsory bytes U per launch, see
-DESIGN.md), cpu_baseline (the oracle port on all host cores), e2e (host
-buffers through gespmm_csr_spmm_host: H2D + validate + plan + kernel + D2H),
-clocks (nvidia-smi sampled during the run), gpu_launches.
+Extra keys: roofline (HBM, algorithmic compulsory bytes U per launch, the
+ncu DRAM traffic of the same kernel, and gather_ceiling: a live gather-only
+replay of the same column stream at the kernel's memory-level parallelism;
+see DESIGN.md), cpu_baseline (the oracle port on all host cores, ~10 s, plus a
+single-thread sample), e2e (host buffers through gespmm_csr_spmm_host:
+pipelined H2D + device colind check + plan + kernel + D2H), clocks (NVML
+samples inside the timed region; the nvidia-smi record rides along),
+sustained (the same steps after a 1 s soak at the power cap), c_allgather
+(N > 1: fused peer-store vs NCCL all-gather of C), gpu_launches.
 
 --impl reference: the reference's own CPU implementation of the path (the
 unmodified raceset interpreter running gespmm_alg2.mir, oracle/_ref) on a
