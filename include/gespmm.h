@@ -234,6 +234,23 @@ gespmm_status_t gespmm_rmat_csr(int32_t scale, int64_t edges, double a, double b
 gespmm_status_t gespmm_uniform_fill(float* out, int64_t n, float lo, float hi, uint64_t seed,
                                     void* stream);
 
+/* ---- format conversions on the GPU (the data formats around the path) ----
+ * COO -> CSR: rows/cols/vals[nnz] (DEVICE) -> rowptr[M+1], colind/vals_out[nnz];
+ * entries keep their input order within a row (stable), duplicates are kept
+ * (the CSR contract allows both; the within-row order is the fold order).
+ * GESPMM_OUT_OF_BOUNDS when a row index lies outside [0, M).  Synchronizes
+ * `stream` once (the range check). */
+gespmm_status_t gespmm_coo_to_csr(int64_t M, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                                  const float* vals, int32_t* rowptr, int32_t* colind, float* vals_out,
+                                  void* stream);
+/* CSR of A (M x K, DEVICE) -> CSR of A^T (K x M): t_rowptr[K+1],
+ * t_colind/t_vals[nnz]; row j of A^T lists column j's nonzeros in ascending
+ * row order (the CSC of A).  GESPMM_OUT_OF_BOUNDS for a column outside
+ * [0, K).  Synchronizes `stream` once. */
+gespmm_status_t gespmm_csr_transpose(int64_t M, int64_t K, int64_t nnz, const int32_t* rowptr,
+                                     const int32_t* colind, const float* vals, int32_t* t_rowptr,
+                                     int32_t* t_colind, float* t_vals, void* stream);
+
 /* ---- multi-GPU (row-block sharding) -------------
  * NCCL is resolved at run time (dlopen "libnccl.so.2"; the copy already loaded
  * in the process wins), so the library never drags in a second NCCL. */

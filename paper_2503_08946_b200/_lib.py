@@ -26,7 +26,7 @@ EXPORTS = [
     "gespmm_plan_execute_peers", "gespmm_ipc_get_handle", "gespmm_ipc_open_handle", "gespmm_ipc_close_handle", "gespmm_plan_get_info",
     "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_set_panel_override",
     "gespmm_panel_width", "gespmm_set_schedule_override", "gespmm_partition_rows",
-    "gespmm_rmat_csr", "gespmm_uniform_fill",
+    "gespmm_rmat_csr", "gespmm_uniform_fill", "gespmm_coo_to_csr", "gespmm_csr_transpose",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
     "gespmm_sharded_spmm_chunked",
 ]
@@ -85,6 +85,8 @@ def load():
         "gespmm_partition_rows": ([_i64, _vp, _int, _vp], _int),
         "gespmm_rmat_csr": ([_int, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                              ctypes.c_uint64, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp], _int),
+        "gespmm_coo_to_csr": ([_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+        "gespmm_csr_transpose": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
         "gespmm_uniform_fill": ([_vp, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_uint64, _vp], _int),
         "gespmm_comm_get_unique_id": ([ctypes.c_char_p], _int),
         "gespmm_comm_init": ([ctypes.POINTER(_vp), _int, ctypes.c_char_p, _int], _int),

@@ -252,6 +252,34 @@ def set_variant_override(name: str = "") -> None:
     _lib.check(_L.gespmm_set_variant_override(name.encode()))
 
 
+def coo_to_csr(rows, cols, vals, M: int, stream=None):
+    """COO (torch CUDA int32 rows/cols, float32 vals) -> (rowptr, colind, vals)
+    CSR on the GPU (gespmm_coo_to_csr): stable by row, duplicates kept."""
+    torch = _torch()
+    nnz = rows.numel()
+    rowptr = torch.empty(M + 1, dtype=torch.int32, device=rows.device)
+    colind = torch.empty(max(nnz, 1), dtype=torch.int32, device=rows.device)
+    v = torch.empty(max(nnz, 1), dtype=torch.float32, device=rows.device)
+    _lib.check(_L.gespmm_coo_to_csr(M, nnz, rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), rowptr.data_ptr(),
+                                    colind.data_ptr(), v.data_ptr(), _stream_handle(stream, rows.device)))
+    return rowptr, colind[:nnz], v[:nnz]
+
+
+def csr_transpose(rowptr, colind, vals, K: int, stream=None):
+    """CSR of A (M x K) -> CSR of A^T (K x M) on the GPU (gespmm_csr_transpose);
+    row j of A^T lists column j's nonzeros in ascending row order."""
+    torch = _torch()
+    M = rowptr.numel() - 1
+    nnz = colind.numel()
+    t_rp = torch.empty(K + 1, dtype=torch.int32, device=rowptr.device)
+    t_ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=rowptr.device)
+    t_v = torch.empty(max(nnz, 1), dtype=torch.float32, device=rowptr.device)
+    _lib.check(_L.gespmm_csr_transpose(M, K, nnz, rowptr.data_ptr(), colind.data_ptr(), vals.data_ptr(),
+                                       t_rp.data_ptr(), t_ci.data_ptr(), t_v.data_ptr(),
+                                       _stream_handle(stream, rowptr.device)))
+    return t_rp, t_ci[:nnz], t_v[:nnz]
+
+
 def ipc_handle(t) -> tuple:
     """(64-byte CUDA IPC handle of the allocation holding tensor t, byte offset
     of t in it) -- for the fused all-gather's peer buffers."""
