@@ -49,6 +49,10 @@ constexpr int kMaxChunks = 16;
 #define GESPMM_DYN 1
 #endif
 constexpr int64_t kDynMinItems = 16384;  // below: static warp striding
+// Long-row segment tickets: acq_rel atomic by one lane (1) or full fences (0).
+#ifndef GESPMM_TICKET_ACQREL
+#define GESPMM_TICKET_ACQREL 1
+#endif
 // Fused all-gather: at most this many destination buffers (one node's GPUs).
 constexpr int kMaxPeers = 8;
 

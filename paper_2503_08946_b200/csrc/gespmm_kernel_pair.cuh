@@ -278,6 +278,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
       combined(o);
       if (storer) Vec<VEC>::st(P.partials + static_cast<int64_t>(slot + seg) * P.ldp + woff, o);
     }
+#if GESPMM_TICKET_ACQREL
+    // the warp's partial stores are ordered before lane 0's release by the
+    // warp barrier; lane 0's acq_rel ticket releases them at gpu scope (and,
+    // for the last segment, acquires the others') -- one lane, no full fence
+    __syncwarp();
+    int ticket = 0;
+    int* counter = P.counters + static_cast<int64_t>(slot) * P.ncb + cb;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(ticket) : "l"(counter) : "memory");
+    ticket = __shfl_sync(FULL, ticket, 0);
+    if (ticket != nseg - 1) GESPMM_NEXT_ITEM;
+    __syncwarp();  // lane 0's acquire orders the whole warp's partial loads below
+#else
     __threadfence();
     __syncwarp();
     int ticket = 0;
@@ -285,9 +298,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     if (lane == 0) ticket = atomicAdd(counter, 1);
     ticket = __shfl_sync(FULL, ticket, 0);
     if (ticket != nseg - 1) GESPMM_NEXT_ITEM;
+#endif
     // last segment: combine the partials strictly left to right (both halves
     // compute it; the lower half stores)
-    __threadfence();
+    if (!GESPMM_TICKET_ACQREL) __threadfence();
     const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp + woff;
     float r[VEC];
     Vec<VEC>::ldcg(r, base);
