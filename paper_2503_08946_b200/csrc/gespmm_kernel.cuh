@@ -462,15 +462,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     } else {
       nr = 1;
       lo = it.z + it.y * kSeg;
-      re_long = __ldg(P.rowptr + it.x + 1);
-      hi = min(lo + kSeg, re_long);
+      re_long = __ldg(P.rowptr + it.x + 1);  // in flight while the stage copy is issued
+      hi = min(lo + kSeg, P.nnz);  // copy bound; the segment end is applied below
     }
     // ---- CRC staging: colind/vals [sbase, hi) -> shared memory -------------
     // Batches start at 4-aligned positions sbase + k*U; entries in [sbase, lo)
     // are real neighbours (valid offsets, never folded) and the pad up to the
     // last batch end is zeroed below (offset 0: a valid row, never folded).
     const int sbase = lo & ~3;
-    const int send = sbase + ((hi - sbase + U - 1) / U) * U;
     if (P.idx_aligned) {
       for (int e = sbase + 4 * lane; e < hi; e += 128) {
         if (e + 4 <= P.nnz) {
@@ -489,6 +488,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         cp_async4(sv + (e - sbase), P.vals + e);
       }
     }
+    // a segment's true end (its row's end) arrives while the copy is in flight
+    // (entries copied past it are never folded: the pad and the batch bound
+    // below stop at `hi`)
+    if (!is_tile) hi = min(lo + kSeg, re_long);
+    const int send = sbase + ((hi - sbase + U - 1) / U) * U;
     cp_async_wait_all();
     __syncwarp();
     // zero the pad [hi, send) (overwrites any neighbours cp.async brought in)

@@ -154,12 +154,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     } else {
       nr = 1;
       lo = it.z + it.y * kSeg;
-      re_long = __ldg(P.rowptr + it.x + 1);
-      hi = min(lo + kSeg, re_long);
+      re_long = __ldg(P.rowptr + it.x + 1);  // in flight while the stage copy is issued
+      hi = min(lo + kSeg, P.nnz);  // copy bound; the segment end is applied below
     }
     // ---- CRC staging (as in gespmm_kernel.cuh), then the parity permutation --
     const int sbase = lo & ~3;
-    const int send = sbase + ((hi - sbase + U - 1) / U) * U;
     if (P.idx_aligned) {
       for (int e = sbase + 4 * lane; e < hi; e += 128) {
         if (e + 4 <= P.nnz) {
@@ -178,6 +177,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
         cp_async4(sv + (e - sbase), P.vals + e);
       }
     }
+    // a segment's true end (its row's end) arrives while the copy is in flight
+    // (entries copied past it are never folded: the pad and the batch bound
+    // below stop at `hi`)
+    if (!is_tile) hi = min(lo + kSeg, re_long);
+    const int send = sbase + ((hi - sbase + U - 1) / U) * U;
     cp_async_wait_all();
     __syncwarp();
     for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;  // pad: row 0, never folded
