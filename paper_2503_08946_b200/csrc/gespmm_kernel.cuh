@@ -153,6 +153,9 @@ __device__ __forceinline__ void gather_off<4>(float* d, const float* base, uint3
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
       : "r"(off), "l"(base), "l"(pol));
 }
+#ifndef GESPMM_MERGED_PAD
+#define GESPMM_MERGED_PAD 1  // pad zeroing folded into the offset pre-scale pass
+#endif
 #ifndef GESPMM_FAST_VEC2
 #define GESPMM_FAST_VEC2 0  // in-row fast batch at two columns per lane (0 = off)
 #endif
@@ -494,21 +497,43 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     if (!is_tile) hi = min(lo + kSeg, re_long);
     const int send = sbase + ((hi - sbase + U - 1) / U) * U;
     cp_async_wait_all();
-    __syncwarp();
-    // zero the pad [hi, send) (overwrites any neighbours cp.async brought in)
-    for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;
-    __syncwarp();
-    if (OFF32) {  // col -> B-row element offset col*ldb, once per staged entry
+    if (!P.idx_aligned) __syncwarp();  // 4-byte copies: other lanes own the entries
+    if (OFF32 && GESPMM_MERGED_PAD) {
+      // one pass: col -> B-row element offset col*ldb, and the pad [hi, send)
+      // -> 0 (offset 0: a valid row, never folded; it overwrites whatever
+      // neighbours cp.async brought in).  Each lane rewrites exactly the 4
+      // entries its own 16-byte copy delivered (cp.async.wait_group orders
+      // them for it), so with 16-byte staging no warp barrier is needed before this pass
+      // (oracle/models/gespmm_b200_stage.model: copy and pre-scale share a
+      // warp phase); the barrier after it publishes the stage.
       const uint32_t ldb32 = static_cast<uint32_t>(ldb);
+      const int pad = hi - sbase;
       for (int i = 4 * lane; i < send - sbase; i += 128) {
         int4 c = *reinterpret_cast<int4*>(sc + i);
-        c.x = static_cast<int>(static_cast<uint32_t>(c.x) * ldb32);
-        c.y = static_cast<int>(static_cast<uint32_t>(c.y) * ldb32);
-        c.z = static_cast<int>(static_cast<uint32_t>(c.z) * ldb32);
-        c.w = static_cast<int>(static_cast<uint32_t>(c.w) * ldb32);
+        c.x = i + 0 < pad ? static_cast<int>(static_cast<uint32_t>(c.x) * ldb32) : 0;
+        c.y = i + 1 < pad ? static_cast<int>(static_cast<uint32_t>(c.y) * ldb32) : 0;
+        c.z = i + 2 < pad ? static_cast<int>(static_cast<uint32_t>(c.z) * ldb32) : 0;
+        c.w = i + 3 < pad ? static_cast<int>(static_cast<uint32_t>(c.w) * ldb32) : 0;
         *reinterpret_cast<int4*>(sc + i) = c;
       }
       __syncwarp();
+    } else {
+      __syncwarp();
+      // zero the pad [hi, send) (overwrites any neighbours cp.async brought in)
+      for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;
+      __syncwarp();
+      if (OFF32) {  // col -> B-row element offset col*ldb, once per staged entry
+        const uint32_t ldb32 = static_cast<uint32_t>(ldb);
+        for (int i = 4 * lane; i < send - sbase; i += 128) {
+          int4 c = *reinterpret_cast<int4*>(sc + i);
+          c.x = static_cast<int>(static_cast<uint32_t>(c.x) * ldb32);
+          c.y = static_cast<int>(static_cast<uint32_t>(c.y) * ldb32);
+          c.z = static_cast<int>(static_cast<uint32_t>(c.z) * ldb32);
+          c.w = static_cast<int>(static_cast<uint32_t>(c.w) * ldb32);
+          *reinterpret_cast<int4*>(sc + i) = c;
+        }
+        __syncwarp();
+      }
     }
 
     // ---- row state ----------------------------------------------------------

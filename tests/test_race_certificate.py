@@ -6,9 +6,10 @@ oracle/models/gespmm_b200_stage.model restates the kernel's item loop
 grammar (/root/reference/proj/include/raceset/model_text.hpp:12-29);
 oracle/_ref/race_cert runs raceset::races() (proj/src/depcheck.cpp:218, warp
 phases proj/src/kernel_model.cpp:328-356) on it.  The protocol must come out
-RACE-FREE, and removing any one of its four __syncwarp() barriers, or sharing
-one stage slice between warps, must come out RACE-FOUND with a witness -- the
-checker sees the protocol, not a vacuous model.
+RACE-FREE, and removing either of its __syncwarp() barriers, giving the
+pre-scale pass a different owner map than the copy, or sharing one stage slice
+between warps, must come out RACE-FOUND with a witness -- the checker sees the
+protocol, not a vacuous model.
 
 The long-row partial combine (atomic ticket + __threadfence) is outside the
 checker's model (no atomics; distinct blocks are never ordered), as are the
@@ -56,10 +57,14 @@ def test_kernel_staging_protocol_is_race_free():
 
 # (mutation, substitutions, expected racing pair on sm_k)
 MUTANTS = [
-    ("no_stage_barrier", [("schedule P = [0, 4*q + 1,", "schedule P = [0, 4*q,")], {"F", "P"}),
-    ("no_pad_barrier", [("schedule X = [0, 4*q + 2,", "schedule X = [0, 4*q + 1,")], {"P", "X"}),
-    ("no_consume_barrier", [("schedule T = [0, 4*q + 3,", "schedule T = [0, 4*q + 2,")], {"X", "T"}),
-    ("no_loop_barrier", [("schedule F = [0, 4*q,", "schedule F = [0, 4*q - 1,")], {"F", "T"}),
+    # the pre-scale pass working on another lane's copied entries (the 4-byte
+    # staging owner map) without the barrier the kernel then inserts
+    ("foreign_owner", [("  read sm_k[8*w + tx + 4*r]\n  write sm_k[8*w + tx + 4*r]\n",
+                        "  read sm_k[8*w + 2*tx + r]\n  write sm_k[8*w + 2*tx + r]\n")], {"F", "X"}),
+    # T then shares the copy's phase too; the checker's first witness is F/T
+    ("no_publish_barrier", [("schedule T = [0, 2*q + 1,", "schedule T = [0, 2*q,")], {"F", "T"}),
+    ("no_loop_barrier", [("schedule F = [0, 2*q,", "schedule F = [0, 2*q - 1,"),
+                         ("schedule X = [0, 2*q,", "schedule X = [0, 2*q - 1,")], {"F", "T"}),
     ("shared_slice", [("sm_k[8*w + ", "sm_k["), ("sm_v[8*w + ", "sm_v[")], {"F"}),
 ]
 
