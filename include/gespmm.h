@@ -32,14 +32,16 @@
  *         from A = 0 (accumulate: C0), B likewise from -0.0; value = A + B
  *   MEAN: the SUM value from A = 0, then / deg(i) (correctly rounded);
  *         accumulate adds C0
- *   MAX/MIN: m = val[p]*B[col[p]][j] (rounded, unfused); acc = first m, then
- *         acc = (m > acc) ? m : acc   (MIN: <); accumulate seeds acc = C0
+ *   MAX/MIN: m = val[p]*B[col[p]][j] (rounded, unfused); the value is IEEE
+ *         754-2019 maximumNumber (MIN: minimumNumber) over the row's messages
+ *         and, with accumulate, C0: NaN operands ignored, all-NaN -> the
+ *         canonical NaN 0x7fffffff, -0 < +0 (the B200's FMNMX); order-free
  *   empty rows give 0 (accumulate: C0 for sum/max/min, C0 + 0 for mean).
  *   Rows with more than GESPMM_SEGMENT_LEN nonzeros are reduced in fixed
  *   GESPMM_SEGMENT_LEN-long segments from the row start (each segment as above,
- *   later segments seeded with 0 / -inf / +inf), combined strictly left to
- *   right (sum/mean: +, max/min: the same comparison).  Results are
- *   deterministic and independent of device, grid and sharding.
+ *   later segments seeded with 0 / NaN), combined left to right (sum/mean: +,
+ *   max/min: maximumNumber/minimumNumber).  Results are deterministic and
+ *   independent of device, grid and sharding.
  */
 #ifndef GESPMM_H_
 #define GESPMM_H_

@@ -22,8 +22,8 @@
  *  2. oracle_spmm_f32 -- the fp32 "twin": the normative fp32 semantics of the
  *     B200 path: fp32 with explicit fused multiply-adds
  *     (fmaf); sum/mean reduce each row (segment) as two ascending FMA chains
- *     over the even- and odd-offset positions, added at the end; max/min fold
- *     in ascending p; long rows (more than seg_len nonzeros) are reduced in
+ *     over the even- and odd-offset positions, added at the end; max/min are
+ *     maximumNumber/minimumNumber over the row's messages; long rows (more than seg_len nonzeros) are reduced in
  *     seg_len-long segments combined left to right.  The GPU result is
  *     bit-identical to this twin.
  *
@@ -103,20 +103,31 @@ void oracle_spmm_absbound_f64(int64_t M, int64_t N, const int32_t* rowptr, const
 
 /* ---- (2) the fp32 twin ---------------------------------------------------- */
 
-/* better(m, acc): the max/min fold step, acc = (m > acc) ? m : acc (for min, <).
- * Products are plain fp32 multiplies; the Makefile builds with
+/* pick(op, a, b): the max/min fold step, IEEE 754-2019 maximumNumber /
+ * minimumNumber (5.3.1) exactly as the B200's FMNMX computes them (measured,
+ * tools/mnmx_probe.cu): a NaN operand is ignored, two NaNs give the canonical
+ * NaN 0x7fffffff, and -0 < +0.  Commutative and associative, so a row's
+ * max/min depends on its message multiset only (the GPU folds two messages
+ * per FMNMX3).  Products are plain fp32 multiplies; the Makefile builds with
  * -ffp-contract=off so they are never contracted into an FMA. */
-static inline float better(int op, float m, float acc) {
-  if (op == OR_MAX) return (m > acc) ? m : acc;
-  return (m < acc) ? m : acc;
+static inline float canonical_nan(void) {
+  union { uint32_t u; float f; } x = {0x7fffffffu};
+  return x.f;
+}
+static inline float pick(int op, float a, float b) {
+  if (isnan(a)) return isnan(b) ? canonical_nan() : b;
+  if (isnan(b)) return a;
+  if (a == b) return (signbit(a) != 0) == (op == OR_MAX) ? b : a; /* +-0 tie; else identical */
+  if (op == OR_MAX) return a > b ? a : b;
+  return a < b ? a : b;
 }
 
 /* Reduce nonzeros [ps, pe) of one row into acc[0..N).  Per column j the order
  * is p ascending, exactly as in the reference (gespmm_alg2.mir:38-59).
- * mode: 0 = first segment without an initial value (max/min take the first
- *           message; sum starts from +0),
+ * mode: 0 = first segment without an initial value (sum: +0; max/min: the
+ *           canonical NaN, maximumNumber's identity),
  *       1 = first segment seeded with init[] (accumulate=1: C0),
- *       2 = later segment (sum: +0; max: -inf; min: +inf). */
+ *       2 = later segment (sum: +0; max/min: the canonical NaN). */
 static void fold_span(int op, int64_t ps, int64_t pe, int64_t N, const int32_t* colind,
                       const float* vals, const float* B, int64_t ldb, int mode,
                       const float* init, float* acc) {
@@ -139,29 +150,21 @@ static void fold_span(int op, int64_t ps, int64_t pe, int64_t N, const int32_t* 
     for (int64_t j = 0; j < N; ++j) acc[j] = acc[j] + accb[j];
     return;
   }
-  if (mode == 0) {
-    const float v = vals[p];
-    const float* b = B + (int64_t)colind[p] * ldb;
-    for (int64_t j = 0; j < N; ++j) acc[j] = v * b[j];
-    ++p;
-  } else {
-    for (int64_t j = 0; j < N; ++j)
-      acc[j] = (mode == 1) ? init[j] : (op == OR_MAX ? -INFINITY : INFINITY);
-  }
+  for (int64_t j = 0; j < N; ++j) acc[j] = (mode == 1) ? init[j] : canonical_nan();
   for (; p < pe; ++p) {
     const float v = vals[p];
     const float* b = B + (int64_t)colind[p] * ldb;
-    if (op == OR_MAX)
-      for (int64_t j = 0; j < N; ++j) { float m = v * b[j]; acc[j] = (m > acc[j]) ? m : acc[j]; }
-    else
-      for (int64_t j = 0; j < N; ++j) { float m = v * b[j]; acc[j] = (m < acc[j]) ? m : acc[j]; }
+    for (int64_t j = 0; j < N; ++j) {
+      const float m = v * b[j];
+      acc[j] = pick(op, acc[j], m);
+    }
   }
 }
 
 /* C = A (op) B, or C = C0 (+) A (op) B with accumulate=1.  seg_len <= 0 means
  * "never split"; otherwise rows with deg > seg_len are reduced per segment
  * [rs + k*seg_len, rs + (k+1)*seg_len) and combined left to right:
- *   sum/mean: acc = acc + part;  max/min: acc = better(part, acc).
+ *   sum/mean: acc = acc + part;  max/min: acc = pick(acc, part).
  * Empty rows: sum/mean/max/min give 0 (accumulate=1: C0). */
 int oracle_spmm_f32(int64_t M, int64_t N, const int32_t* rowptr, const int32_t* colind,
                     const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc, int op,
@@ -194,7 +197,7 @@ int oracle_spmm_f32(int64_t M, int64_t N, const int32_t* rowptr, const int32_t* 
         for (int64_t s = e0; s < re; s += seg_len) {
           int64_t e = s + seg_len < re ? s + seg_len : re;
           fold_span(op, s, e, N, colind, vals, B, ldb, 2, c0, part);
-          for (int64_t j = 0; j < N; ++j) acc[j] = better(op, part[j], acc[j]);
+          for (int64_t j = 0; j < N; ++j) acc[j] = pick(op, acc[j], part[j]);
         }
         for (int64_t j = 0; j < N; ++j) out[j] = acc[j];
       } else {

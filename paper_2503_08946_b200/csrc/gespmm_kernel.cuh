@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
 
   // acc[slot] += v * b per the semiring; sum/mean column pairs go through
   // FFMA2 (Blackwell's packed fp32 FMA: two independent RN FMAs, bit-identical)
-  auto fold = [&](int slot, float v, const float (&bb)[CWM][VEC], bool first) {
+  auto fold = [&](int slot, float v, const float (&bb)[CWM][VEC]) {
     float (&a)[CWM][VEC] = acc[TWO ? slot : 0];
 #pragma unroll
     for (int w = 0; w < CWM; ++w) {
@@ -403,8 +403,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         for (int k = 0; k < VEC; k += 2) fma2_rn(a[w][k], a[w][k + 1], v, bb[w][k], bb[w][k + 1]);
       } else {
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) a[w][k] = SR::update(a[w][k], v, bb[w][k], first);
+        for (int k = 0; k < VEC; ++k) a[w][k] = SR::update(a[w][k], v, bb[w][k]);
       }
+    }
+  };
+  // Two consecutive messages at once (sum/mean: the two chains; max/min: the
+  // products in FMUL2 and one FMNMX3 per column -- the order-free fold).
+  auto fold_pair = [&](float v0, const float (&b0)[CWM][VEC], float v1, const float (&b1)[CWM][VEC]) {
+    if constexpr (SR::kMnmx) {
+      float(&a)[CWM][VEC] = acc[0];
+#pragma unroll
+      for (int w = 0; w < CWM; ++w) {
+        if constexpr (VEC >= 2) {
+#pragma unroll
+          for (int k = 0; k < VEC; k += 2) {
+            float m0, m1, n0, n1;
+            mul2_rn(m0, m1, v0, b0[w][k], b0[w][k + 1]);
+            mul2_rn(n0, n1, v1, b1[w][k], b1[w][k + 1]);
+            a[w][k] = SR::pick3(a[w][k], m0, n0);
+            a[w][k + 1] = SR::pick3(a[w][k + 1], m1, n1);
+          }
+        } else {
+          a[w][0] = SR::pick3(a[w][0], __fmul_rn(v0, b0[w][0]), __fmul_rn(v1, b1[w][0]));
+        }
+      }
+    } else {
+      fold(0, v0, b0);
+      fold(1, v1, b1);
     }
   };
 
@@ -541,9 +566,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     const int64_t ldc = P.ldc;
     float* crow = P.C + grow0 * ldc + woff[0];
     int row = 0, rs = lo, re = is_tile ? rp[1] : hi;
-    // max/min take their first message as the initial value, except when
-    // seeded (accumulate) or in a later segment (seeded with the identity).
-    const bool first_ok = SR::kFirstMsg && !accumulate && (is_tile || it.y == 0);
     if (!is_tile && it.y > 0) seed(lo, SR::identity(), nullptr);
     else row_seed(lo, crow);
 
@@ -594,9 +616,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         v[4 * g] = x.x, v[4 * g + 1] = x.y, v[4 * g + 2] = x.z, v[4 * g + 3] = x.w;
       }
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
-        const bool first = first_ok && qb == rs;
 #pragma unroll
-        for (int u = 0; u < U; ++u) fold(u & 1, v[u], b[u], first && u == 0);
+        for (int u = 0; u < U; u += 2) fold_pair(v[u], b[u], v[u + 1], b[u + 1]);
         return;
       }
 #pragma unroll
@@ -611,7 +632,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
           re = rp[row + 1];
           row_seed(rs, crow);
         }
-        fold(u & 1, v[u], b[u], first_ok && p == rs);
+        fold(u & 1, v[u], b[u]);
       }
     };
     if (RING && lo < hi) {
@@ -656,14 +677,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
                 gather(bf[4 * g + 3], o.w);
               }
               const float4* vp = reinterpret_cast<const float4*>(sv + (qb - sbase));
-              const bool first = first_ok && qb == rs;
 #pragma unroll
               for (int g = 0; g < FB / 4; ++g) {
                 const float4 x = vp[g];
-                fold(0, x.x, bf[4 * g + 0], first && g == 0);
-                fold(1, x.y, bf[4 * g + 1], false);
-                fold(0, x.z, bf[4 * g + 2], false);
-                fold(1, x.w, bf[4 * g + 3], false);
+                fold_pair(x.x, bf[4 * g + 0], x.y, bf[4 * g + 1]);
+                fold_pair(x.z, bf[4 * g + 2], x.w, bf[4 * g + 3]);
               }
               qb += FB;
             }

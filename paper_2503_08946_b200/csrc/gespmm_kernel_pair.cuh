@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
 #pragma unroll
       for (int k = 0; k < VEC; k += 2) fma2_rn(acc[k], acc[k + 1], v, b[k], b[k + 1]);
     } else {
-      acc[0] = SR::update(acc[0], v, b[0], false);
+      acc[0] = SR::update(acc[0], v, b[0]);
     }
   };
 

@@ -1,8 +1,11 @@
-# A/B: every built lib on workload/op pairs: scripts/gpu_ab_op.sh W:OP [W:OP ...]
+# A/B every built lib on (workload, op) pairs given as workload:op (kernel only),
+# after the GPU test suite with the default lib.
 mkdir -p gpurun_out
+export GESPMM_NO_PROBE=1
 timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
-for wo in "$@"; do w=${wo%%:*}; op=${wo##*:}
+for wo in "$@"; do
+w=${wo%%:*}; op=${wo##*:}
 for lib in paper_2503_08946_b200/libgespmm*.so; do
   b=$(basename $lib .so)
-  GESPMM_LIB=$PWD/$lib timeout 300 python bench.py --workload $w --op $op --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-clocks --soak-s 0 --sustained-s 0 > gpurun_out/ab_${w}_${op}_${b}.log 2>&1
+  GESPMM_LIB=$PWD/$lib timeout 300 python bench.py --workload $w --op $op --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-clocks --soak-s 0 --sustained-s 0 > gpurun_out/abop_${w}_${op}_${b}.log 2>&1
 done; done

@@ -206,6 +206,36 @@ def test_max_min_special_values(cuda, oracle_mod):
         np.testing.assert_array_equal(got[~nan].view(np.uint32), want[~nan].view(np.uint32))
 
 
+@pytest.mark.parametrize("N", [1, 5, 16, 32, 64, 100, 128, 256])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_max_min_maximum_number_all_bits(cuda, oracle_mod, N, accumulate):
+    """max/min = maximumNumber/minimumNumber (FMNMX): every bit equal to the
+    twin, NaNs included (an all-NaN row is the canonical 0x7fffffff on both
+    sides), across every kernel variant N selects, long rows and accumulate."""
+    rng = np.random.default_rng(100 + N)
+    M, K = 400, 96
+    rowptr, colind, vals = random_csr(rng, M, K, 0.1, long_rows=[(1, 900), (2, 300)], empty_frac=0.1)
+    vals[::7] = np.nan
+    vals[1::11] = 0.0
+    vals[2::13] = -0.0
+    vals[3::17] = np.inf
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    B[::5] = -0.0
+    B[1::9] = -np.inf
+    B[2::10] = 0.0
+    # rows whose messages are all NaN / all +-0
+    for r, v in ((3, np.nan), (4, 0.0), (5, -0.0)):
+        vals[rowptr[r]:rowptr[r + 1]] = v
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32) if accumulate else None
+    if accumulate:
+        C0[::6] = np.nan
+        C0[1::8] = -0.0
+    for op in ("max", "min"):
+        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op, C0=C0)
+        want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=accumulate, C0=C0, seg_len=SEG)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 def test_segmented_max_equals_unsegmented(cuda, oracle_mod):
     """Max/min are independent of the long-row split (proved in DESIGN.md)."""
     rng = np.random.default_rng(9)

@@ -1,6 +1,6 @@
 """CPU tier: the fp32 twin (the normative semantics the GPU is bit-exact to)
 checked against a pure-Python restatement on small cases, plus the algebraic
-properties DESIGN.md relies on (segmentation invariance of max/min, mean =
+properties DESIGN.md relies on (order/segmentation invariance of max/min, mean =
 sum/deg, accumulate = the reference's C read-modify-write order)."""
 import math
 from fractions import Fraction
@@ -31,6 +31,21 @@ def fma32(a, b, c):
     cands = [x, np.nextafter(x, np.float32(np.inf)), np.nextafter(x, np.float32(-np.inf))]
     cands = [y for y in cands if math.isfinite(float(y))]
     return min(cands, key=lambda y: (abs(Fraction(float(y)) - exact), int(np.float32(y).view(np.uint32)) & 1))
+
+
+CANON_NAN = np.array([0x7FFFFFFF], np.uint32).view(np.float32)[0]
+
+
+def pick(op, a, b):
+    """IEEE 754-2019 maximumNumber / minimumNumber as the B200's FMNMX computes
+    them: NaN operands ignored, NaN+NaN -> canonical NaN, -0 < +0."""
+    if np.isnan(a):
+        return CANON_NAN if np.isnan(b) else b
+    if np.isnan(b):
+        return a
+    if a == b:  # +-0 tie (equal non-zeros are identical)
+        return b if bool(np.signbit(a)) == (op == "max") else a
+    return (a if a > b else b) if op == "max" else (a if a < b else b)
 
 
 def py_twin(rowptr, colind, vals, B, op, accumulate=False, C0=None, seg=0):
@@ -66,20 +81,12 @@ def py_twin(rowptr, colind, vals, B, op, accumulate=False, C0=None, seg=0):
                 else:
                     C[i, j] = acc_total
             else:
-                better = (lambda m, a: m if m > a else a) if op == "max" else (lambda m, a: m if m < a else a)
                 if deg == 0:
                     C[i, j] = c0 if accumulate else f32(0)
                     continue
-                acc = None
-                for k, (a, b) in enumerate(segs):
-                    if k == 0:
-                        part = c0 if accumulate else None
-                    else:
-                        part = f32(-np.inf) if op == "max" else f32(np.inf)
-                    for p in range(a, b):
-                        m = f32(vals[p] * B[colind[p], j])
-                        part = m if part is None else better(m, part)
-                    acc = part if acc is None else better(part, acc)
+                acc = c0 if accumulate else CANON_NAN
+                for p in range(rs, re):  # order-free: segments do not matter
+                    acc = pick(op, acc, f32(vals[p] * B[colind[p], j]))
                 C[i, j] = acc
     return C
 
@@ -169,3 +176,42 @@ def test_empty_rows_give_zero(oracle_mod):
     for op in ("sum", "max", "min", "mean"):
         got = oracle_mod.spmm_f32(rowptr, np.zeros(0, np.int32), np.zeros(0, np.float32), B, op)
         np.testing.assert_array_equal(got, np.zeros((2, 4), np.float32))
+
+
+def _bits(x):
+    return np.asarray(x, np.float32).view(np.uint32)
+
+
+def test_max_min_are_maximum_number(oracle_mod):
+    """max/min = IEEE 754-2019 maximumNumber/minimumNumber over the messages:
+    NaN messages ignored, all-NaN -> canonical NaN, -0 < +0, order-free."""
+    B = np.array([[1.0], [-0.0], [np.nan], [0.0]], np.float32)
+    one = np.float32(1.0)
+    cases = [  # (columns of the row's messages (vals all 1), max, min)
+        ([1, 3], 0.0, -0.0), ([3, 1], 0.0, -0.0),           # +-0 either order
+        ([2, 0], 1.0, 1.0), ([0, 2], 1.0, 1.0),             # NaN first or last: ignored
+        ([2, 2], CANON_NAN, CANON_NAN), ([2], CANON_NAN, CANON_NAN),
+        ([1], -0.0, -0.0), ([1, 2, 3, 0], 1.0, -0.0),
+    ]
+    for cols, want_max, want_min in cases:
+        rowptr = np.array([0, len(cols)], np.int32)
+        colind = np.array(cols, np.int32)
+        vals = np.full(len(cols), one, np.float32)
+        for op, want in (("max", want_max), ("min", want_min)):
+            got = oracle_mod.spmm_f32(rowptr, colind, vals, B, op)
+            assert _bits(got[0, 0]) == _bits(want), (cols, op, got[0, 0], want)
+            assert _bits(got[0, 0]) == _bits(py_twin(rowptr, colind, vals, B, op)[0, 0])
+
+
+@pytest.mark.parametrize("op", ["max", "min"])
+def test_max_min_independent_of_order(oracle_mod, op):
+    """Permuting each row's nonzeros changes nothing, bit for bit (NaN included)."""
+    rng = np.random.default_rng(11)
+    rowptr, colind, vals, B, C0 = rand_case(5, M=50, K=40, N=7, long_deg=300, special=True)
+    a = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=16)
+    for i in range(len(rowptr) - 1):
+        rs, re = rowptr[i], rowptr[i + 1]
+        perm = rs + rng.permutation(re - rs)
+        colind[rs:re], vals[rs:re] = colind[perm].copy(), vals[perm].copy()
+    b = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=0)
+    np.testing.assert_array_equal(_bits(a), _bits(b))
