@@ -93,8 +93,7 @@ Variant pick_variant(int64_t N, const float* B, int64_t ldb, const float* C, int
   Variant v = choose_variant(N, B, ldb, C, ldc, op);
   if (!g_variant_override.empty()) {
     Variant o;
-    const bool two_chain = op == GESPMM_REDUCE_SUM || op == GESPMM_REDUCE_MEAN;
-    if (parse_variant(g_variant_override.c_str(), &o) && (!o.pair || two_chain)) {
+    if (parse_variant(g_variant_override.c_str(), &o)) {
       auto ok = [&](int vec) {
         const uintptr_t a = static_cast<uintptr_t>(vec) * 4;
         return reinterpret_cast<uintptr_t>(B) % a == 0 && reinterpret_cast<uintptr_t>(C) % a == 0 &&

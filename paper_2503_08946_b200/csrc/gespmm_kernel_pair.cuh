@@ -1,17 +1,19 @@
-// gespmm_kernel_pair.cuh -- paired-lane GE-SpMM kernel for sum/mean at N <= 64.
+// gespmm_kernel_pair.cuh -- paired-lane GE-SpMM kernel for N < 32 (all ops).
 //
 // Same work items, staging and row walk as gespmm_kernel.cuh (read that file
 // first); what differs is the lane mapping.  The sum/mean contract reduces each
 // row (segment) as two FMA chains -- the nonzeros at even and at odd offsets
-// from its start -- added at the end.  Here the two
-// chains live in the two 16-lane halves of the warp: half g folds the staged
-// positions of absolute parity g, each lane owning VEC (<= 4) consecutive
-// columns, so every warp instruction gathers two B rows (two 128-bit loads per
-// lane pair at N=64) and the address math / load count per nonzero halve
-// compared with the 32-lane kernel.  Row control stays warp-uniform (both
-// halves walk the same rows); at a row end the halves' chains are added with one
-// shfl_xor(16) -- fp32 addition is commutative, so both halves hold the same
-// bits -- and the lower half stores.
+// from its start -- added at the end; max/min have no
+// fold order at all (maximumNumber), so any split of the positions works.
+// Here the two chains live in the two 16-lane halves of the warp: half g folds
+// the staged positions of absolute parity g, each lane owning VEC (<= 4)
+// consecutive columns, so every warp instruction gathers two B rows (two
+// 128-bit loads per lane pair at N=64) and the address math / load count per
+// nonzero halve compared with the 32-lane kernel.  Row control stays
+// warp-uniform (both halves walk the same rows); at a row end the halves'
+// chains are combined with one shfl_xor(16) -- fp32 addition and
+// maximumNumber are commutative, so both halves hold the same bits -- and the
+// lower half stores.
 //
 // The stage is permuted per 8-entry block to [0,2,4,6,1,3,5,7] so a half reads
 // its four (col, val) pairs of a batch with one 128-bit shared load each.
@@ -32,7 +34,7 @@ template <gespmm_reduce_t OP, int VEC, bool OFF32>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     spmm_pair_kernel(const KParams P) {
   using SR = Semiring<OP>;
-  static_assert(SR::kFma2, "paired lanes implement the two-chain (sum/mean) contract only");
+  static_assert(SR::kFma2 || SR::kMnmx, "paired lanes: two-chain sum/mean or order-free max/min");
   constexpr int U = GESPMM_PAIR_U;  // positions per batch (U/2 per half; 8 or 16)
   constexpr int H = U / 2;
   constexpr int TW = 16 * VEC;   // columns per column block
@@ -62,26 +64,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
 
   float acc[VEC];
   // chain A (even offsets from `start`) is held by the half whose parity is
-  // start's; it gets x (or C0), the other half -0.0.
+  // start's; it gets x (or C0), the other half the chain identity (sum: -0.0,
+  // max/min: NaN).
   auto seed = [&](int start, float x, const float* src) {
     float c[VEC];
     if (src) Vec<VEC>::ld(c, src);
     const bool mine = g == (start & 1);
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) acc[k] = mine ? (src ? c[k] : x) : -0.0f;
+    for (int k = 0; k < VEC; ++k) acc[k] = mine ? (src ? c[k] : x) : SR::chain_seed();
   };
   auto row_seed = [&](int start, const float* crow_) {
     seed(start, SR::zero(), seed_c0 ? crow_ : nullptr);
   };
-  // A + B across the halves (both halves end with the same bits)
+  // A (+) B across the halves (both halves end with the same bits)
   auto combined = [&](float (&o)[VEC]) {
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) o[k] = acc[k] + __shfl_xor_sync(FULL, acc[k], 16);
+    for (int k = 0; k < VEC; ++k) o[k] = SR::combine(acc[k], __shfl_xor_sync(FULL, acc[k], 16));
   };
   auto store_row = [&](float* dst, int deg) {
     float o[VEC];
     combined(o);
-    if (!storer) return;
+    // max/min over an empty row with accumulate: C0 untouched (the halves'
+    // combine would canonicalize a NaN C0)
+    if (!storer || (SR::kMnmx && accumulate && deg == 0)) return;
     float c0[VEC];
     if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst);
 #pragma unroll
@@ -94,11 +99,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     else Vec<VEC>::ldg(d, bw + static_cast<int64_t>(x) * ldb);
   };
   auto fold = [&](float v, const float (&b)[VEC]) {
-    if (VEC >= 2) {
+    if (SR::kFma2 && VEC >= 2) {
 #pragma unroll
       for (int k = 0; k < VEC; k += 2) fma2_rn(acc[k], acc[k + 1], v, b[k], b[k + 1]);
     } else {
-      acc[0] = SR::update(acc[0], v, b[0]);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[k] = SR::update(acc[k], v, b[k]);
+    }
+  };
+  // two of my half's entries (max/min: products in FMUL2, one FMNMX3 per column)
+  auto fold_pair = [&](float v0, const float (&b0)[VEC], float v1, const float (&b1)[VEC]) {
+    if constexpr (SR::kMnmx) {
+      if constexpr (VEC >= 2) {
+#pragma unroll
+        for (int k = 0; k < VEC; k += 2) {
+          float m0, m1, n0, n1;
+          mul2_rn(m0, m1, v0, b0[k], b0[k + 1]);
+          mul2_rn(n0, n1, v1, b1[k], b1[k + 1]);
+          acc[k] = SR::pick3(acc[k], m0, n0);
+          acc[k + 1] = SR::pick3(acc[k + 1], m1, n1);
+        }
+      } else {
+        acc[0] = SR::pick3(acc[0], __fmul_rn(v0, b0[0]), __fmul_rn(v1, b1[0]));
+      }
+    } else {
+      fold(v0, b0);
+      fold(v1, b1);
     }
   };
 
@@ -242,7 +268,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
       }
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: the batch is in the current row
 #pragma unroll
-        for (int i = 0; i < H; ++i) fold(v[i], b[i]);
+        for (int i = 0; i < H; i += 2) fold_pair(v[i], b[i], v[i + 1], b[i + 1]);
         continue;
       }
 #pragma unroll
@@ -303,8 +329,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     ticket = __shfl_sync(FULL, ticket, 0);
     if (ticket != nseg - 1) GESPMM_NEXT_ITEM;
 #endif
-    // last segment: combine the partials strictly left to right (both halves
-    // compute it; the lower half stores)
+    // last segment: combine the partials left to right (both halves compute
+    // it; the lower half stores)
     if (!GESPMM_TICKET_ACQREL) __threadfence();
     const float* base = P.partials + static_cast<int64_t>(slot) * P.ldp + woff;
     float r[VEC];

@@ -87,6 +87,7 @@ struct Semiring<GESPMM_REDUCE_SUM> {
   static constexpr bool kMnmx = false;
   __device__ __forceinline__ static float zero() { return 0.0f; }
   __device__ __forceinline__ static float identity() { return 0.0f; }
+  __device__ __forceinline__ static float chain_seed() { return -0.0f; }  // chain B: exact identity
   __device__ __forceinline__ static float update(float acc, float v, float b) {
     return __fmaf_rn(v, b, acc);
   }
@@ -103,6 +104,7 @@ struct Semiring<GESPMM_REDUCE_MEAN> {
   static constexpr bool kMnmx = false;
   __device__ __forceinline__ static float zero() { return 0.0f; }
   __device__ __forceinline__ static float identity() { return 0.0f; }
+  __device__ __forceinline__ static float chain_seed() { return -0.0f; }  // chain B: exact identity
   __device__ __forceinline__ static float update(float acc, float v, float b) {
     return __fmaf_rn(v, b, acc);
   }
@@ -122,6 +124,7 @@ struct SemiringMnmx {
   static constexpr bool kMnmx = true;  // two messages per FMNMX3, products in FMUL2
   __device__ __forceinline__ static float identity() { return __int_as_float(0x7fffffff); }
   __device__ __forceinline__ static float zero() { return identity(); }
+  __device__ __forceinline__ static float chain_seed() { return identity(); }
   __device__ __forceinline__ static float pick(float a, float b) { return MAX ? maxnum(a, b) : minnum(a, b); }
   __device__ __forceinline__ static float pick3(float a, float b, float c) {
     return MAX ? maxnum3(a, b, c) : minnum3(a, b, c);

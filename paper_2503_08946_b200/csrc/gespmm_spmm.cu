@@ -38,7 +38,6 @@ const Variant kVariants[] = {{4, 1, false, false}, {4, 2, false, false}, {2, 1, 
                              {2, 2, false, false}, {1, 1, false, false}, {1, 2, false, false},
                              {4, 1, true, false},  {2, 1, true, false},  {1, 1, true, false},
                              {4, 1, false, true},  {2, 1, false, true}};
-bool two_chain(gespmm_reduce_t op) { return op == GESPMM_REDUCE_SUM || op == GESPMM_REDUCE_MEAN; }
 }  // namespace
 
 bool parse_variant(const char* name, Variant* v) {
@@ -51,10 +50,9 @@ bool parse_variant(const char* name, Variant* v) {
 }
 
 // Tile shape selected by N and op (north star item (1)): fewest idle lanes,
-// then fewest column blocks, then the table order above (the paired-lane
-// kernel is sum/mean only).
+// then fewest column blocks, then the table order above.
 Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc,
-                       gespmm_reduce_t op) {
+                       gespmm_reduce_t /*op: every variant implements every op*/) {
   auto aligned = [&](int vec) {
     const uintptr_t a = static_cast<uintptr_t>(vec) * 4;
     return reinterpret_cast<uintptr_t>(B) % a == 0 && reinterpret_cast<uintptr_t>(C) % a == 0 &&
@@ -63,7 +61,7 @@ Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, i
   Variant best{1, 1, false};
   int64_t best_idle = -1, best_ncb = 0;
   for (const Variant& c : kVariants) {
-    if (!aligned(c.vec) || (c.pair && !two_chain(op)) || c.ring) continue;
+    if (!aligned(c.vec) || c.ring) continue;
     const int64_t cols = variant_cols(c);
     const int64_t ncb = (N + cols - 1) / cols;
     const int64_t idle = ncb * cols - N;

@@ -101,20 +101,19 @@ def test_partition_rows_balanced_and_contiguous():
 def test_variant_selection_by_N():
     from paper_2503_08946_b200.spmm import variant_name
 
-    # sum/mean: the paired-lane kernel where 32 lanes would idle
+    # the paired-lane kernel where 32 lanes would idle (every op)
     assert variant_name(16) == "pair_vec1"
     assert variant_name(16, reduce="mean") == "pair_vec1"
+    assert variant_name(16, reduce="max") == "pair_vec1"
     assert variant_name(32) == "vec1_lpr32_cwm1"
     assert variant_name(64) == "vec2_lpr32_cwm1"
     assert variant_name(128) == "vec4_lpr32_cwm1_ring"  # the shared-memory gather ring at 512-byte rows
     assert variant_name(256) == "vec4_lpr32_cwm2"
     assert variant_name(512) == "vec4_lpr32_cwm2"
     assert variant_name(33) == "pair_vec1"  # 3 blocks of 16: 15 idle columns vs 31
-    # max/min keep the sequential 32-lane kernel
-    assert variant_name(16, reduce="max") == "vec1_lpr32_cwm1"
     assert variant_name(32, reduce="min") == "vec1_lpr32_cwm1"
     assert variant_name(64, reduce="max") == "vec2_lpr32_cwm1"
-    assert variant_name(33, reduce="max") == "vec1_lpr32_cwm2"
+    assert variant_name(33, reduce="max") == "pair_vec1"
 
 
 def test_cuda_path_fails_loudly_without_gpu():

@@ -166,7 +166,7 @@ def test_column_panels_bit_exact(cuda, oracle_mod, op, N, panel):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-@pytest.mark.parametrize("op", ["sum", "max"])
+@pytest.mark.parametrize("op", ["sum", "max", "min"])
 def test_every_variant_bit_exact(cuda, oracle_mod, variant, op):
     from paper_2503_08946_b200 import spmm
 
