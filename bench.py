@@ -62,6 +62,7 @@ def parse_args():
     ap.add_argument("--sustained-s", type=float, default=1.0,
                     help="soak length of the extra 'sustained' leg (0 = skip)")
     ap.add_argument("--variant", default="", help="kernel variant override (testing), e.g. vec1_lpr32_cwm2")
+    ap.add_argument("--tile-work", type=int, default=0, help="plan tile size override (tuning); 0 = automatic")
     ap.add_argument("--ref-sample-products", type=int, default=800_000,
                     help="--impl reference: nnz*N products per step (bounds interpreter RAM)")
     return ap.parse_args()
@@ -440,6 +441,9 @@ def main():
     N = spec["N"]
     if args.variant:
         set_variant_override(args.variant)
+    if args.tile_work:
+        from paper_2503_08946_b200.spmm import set_tile_work_override
+        set_tile_work_override(args.tile_work)
     csr, B = make_workload(spec, dev)
     M_all, K, nnz_all = csr.M, csr.K, csr.nnz
     stream = torch.cuda.current_stream(dev)

@@ -211,6 +211,12 @@ gespmm_status_t gespmm_set_panel_override(int64_t cols);
  * static, 1 = dynamic.  Results are identical either way.  Test/tuning
  * knob; not thread-safe. */
 gespmm_status_t gespmm_set_schedule_override(int mode);
+/* Tile size of plans built after the call, in work units (a row costs deg +
+ * 2): 0 = automatic (the largest power of two in [16, 256] that still gives
+ * every warp slot of the GPU work; 256 for large matrices), or a forced value
+ * in [2, 256].  Results are identical for every value (rows stay whole).
+ * Test/tuning knob; not thread-safe. */
+gespmm_status_t gespmm_set_tile_work_override(int32_t units);
 /* The panel width gespmm_plan_execute uses for a K-row B with N columns: one
  * kernel launch per panel, ceil(N / width) launches per execute. */
 int64_t gespmm_panel_width(int64_t K, int64_t N);

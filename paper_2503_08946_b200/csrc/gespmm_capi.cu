@@ -29,6 +29,7 @@ cudaError_t row_item_range(const gespmm_plan_s* plan, const int64_t* rows, int64
 cudaError_t validate_colind_async(const int* colind, int64_t p0, int64_t p1, int64_t K, int* err,
                                   cudaStream_t s);
 std::string csr_error_message(int err, int64_t K);
+extern int g_tile_work_override;
 
 namespace {
 thread_local std::string g_last_error;
@@ -503,7 +504,7 @@ gespmm_status_t gespmm_plan_get_info(gespmm_plan_t plan, gespmm_plan_info_t* inf
   info->n_long_rows = plan->n_long;
   info->n_segments = plan->n_segs;
   info->segment_len = kSeg;
-  info->tile_work = kTileWork;
+  info->tile_work = plan->tile_work;
   info->kernel_launches_per_execute = plan->n_items > 0 ? 1 : 0;
   return GESPMM_OK;
 }
@@ -716,6 +717,13 @@ int64_t gespmm_panel_width(int64_t K, int64_t N) { return N < 1 ? 0 : panel_widt
 gespmm_status_t gespmm_set_schedule_override(int mode) {
   if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: schedule mode -1/0/1");
   g_schedule_override = mode;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_set_tile_work_override(int32_t units) {
+  if (units != 0 && (units < kRowCost || units > kTileWork))
+    return fail(GESPMM_INVALID_ARG, "invalid argument: tile work must be 0 (auto) or in [2, 256]");
+  g_tile_work_override = units;
   return GESPMM_OK;
 }
 

@@ -14,9 +14,14 @@ namespace gespmm {
 // ---- work decomposition constants ------------------------
 // Long rows (deg > kSeg) are cut into kSeg-long segments from the row start.
 constexpr int kSeg = GESPMM_SEGMENT_LEN;
-// A tile is a run of consecutive short rows worth ~kTileWork work units, where a
+// A tile is a run of consecutive short rows worth ~tile_work work units, where a
 // row costs deg + kRowCost (the row cost accounts for its C-row store).
+// tile_work is a power of two in [kMinTileWork, kTileWork], chosen per plan
+// from (nnz, M) alone (never the device): the largest one that still gives
+// every warp slot of a 148-SM B200 (x2) an item, so small matrices are not
+// latency-bound on a few long warps (tile_work_for).
 constexpr int kTileWork = 256;
+constexpr int kMinTileWork = 16;
 constexpr int kRowCost = 2;
 // Rows per tile are bounded: every short row advances the work prefix by >= kRowCost.
 constexpr int kTileMaxRows = kTileWork / kRowCost;
@@ -139,5 +144,6 @@ struct gespmm_plan_s {
   unsigned long long* work_ctr = nullptr;  // per column block item counters (GESPMM_DYN)
   int64_t work_ctr_n = 0;  // [2] items of the current execute_rows chunk (+ a zero abort flag)
   int64_t counter_ints = 0;
+  int tile_work = gespmm::kTileWork;
   int device = 0;
 };

@@ -6,9 +6,10 @@
 // Output: a list of work items, one warp each, in row order:
 //   TILE    {r0, -1, rowptr[r0], 0}: consecutive short rows (deg <= kSeg); the
 //           tile ends where the next item starts.  A short row costs
-//           w = deg + kRowCost work units; row i joins tile floor(E_i / kTileWork)
-//           where E is the exclusive prefix of w, so a tile holds ~kTileWork
-//           units (<= kTileWork + kSeg + kRowCost) and <= kTileMaxRows rows.
+//           w = deg + kRowCost work units; row i joins tile floor(E_i / tw)
+//           where E is the exclusive prefix of w and tw the plan's tile_work,
+//           so a tile holds ~tw units (<= tw + kSeg + kRowCost) and <= tw /
+//           kRowCost rows.
 //   SEGMENT {row, s, rowptr[row], slot}: nonzeros [rs + s*kSeg, rs + (s+1)*kSeg)
 //           of a long row; `slot` is the row's first partial-buffer slot.
 // A long row always ends the tile before it.  The decomposition depends only
@@ -62,30 +63,30 @@ __global__ void k_colind(const int* __restrict__ colind, int64_t nnz, int K, int
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrColRange);
 }
 
-__device__ __forceinline__ bool tile_start(int i, const uint64_t* packed, const uint64_t* E) {
+__device__ __forceinline__ bool tile_start(int i, const uint64_t* packed, const uint64_t* E, int tw) {
   const uint64_t pi = packed[i];
   if ((pi & kLowMask) == 0) return false;  // long row: no tile starts here
   if (i == 0) return true;
   const uint64_t pp = packed[i - 1];
   if ((pp & kLowMask) == 0) return true;   // previous row is long
-  return ((E[i] & kLowMask) / kTileWork) != ((E[i - 1] & kLowMask) / kTileWork);
+  return ((E[i] & kLowMask) / tw) != ((E[i - 1] & kLowMask) / tw);
 }
 
-__global__ void k_count(const uint64_t* __restrict__ packed, const uint64_t* __restrict__ E, int M,
+__global__ void k_count(const uint64_t* __restrict__ packed, const uint64_t* __restrict__ E, int M, int tw,
                         int* __restrict__ cnt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M) return;
-  cnt[i] = (tile_start(i, packed, E) ? 1 : 0) + static_cast<int>(packed[i] >> kPackShift);
+  cnt[i] = (tile_start(i, packed, E, tw) ? 1 : 0) + static_cast<int>(packed[i] >> kPackShift);
 }
 
 __global__ void k_emit(const int* __restrict__ rowptr, const uint64_t* __restrict__ packed,
-                       const uint64_t* __restrict__ E, const int* __restrict__ pos, int M,
+                       const uint64_t* __restrict__ E, const int* __restrict__ pos, int M, int tw,
                        int4* __restrict__ items) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M) return;
   int p = pos[i];
   const int rs = rowptr[i];
-  if (tile_start(i, packed, E)) items[p++] = make_int4(i, -1, rs, 0);
+  if (tile_start(i, packed, E, tw)) items[p++] = make_int4(i, -1, rs, 0);
   const int ns = static_cast<int>(packed[i] >> kPackShift);
   const int slot = static_cast<int>(E[i] >> kPackShift);
   for (int s = 0; s < ns; ++s) items[p++] = make_int4(i, s, rs, slot);
@@ -179,6 +180,22 @@ cudaError_t validate_colind_async(const int* colind, int64_t p0, int64_t p1, int
 }
 
 std::string csr_error_message(int err, int64_t K) { return csr_error_text(err, K); }
+
+int g_tile_work_override = 0;  // > 0: forced tile_work (tests/tuning)
+
+// The plan's tile_work: the largest power of two in [kMinTileWork, kTileWork]
+// with at least 2 x 148 x 32 tiles' worth of work (148 SMs x 32 resident
+// warps), from (nnz, M) only so the decomposition stays device-independent.
+// Results never depend on it (short rows stay whole).  Measured on config 1
+// (4096^2, 168 K nnz, picks 16): 256 / 64 / 32 / 16 / 8 units -> 20.3 / 12.5 /
+// 12.3 / 11.6 / 11.5 us; config 3 (picks 256) within 1 % for 16..256.
+int tile_work_for(int64_t M, int64_t nnz) {
+  if (g_tile_work_override > 0) return g_tile_work_override;
+  const int64_t work = nnz + kRowCost * M;
+  int tw = kTileWork;
+  while (tw > kMinTileWork && work < static_cast<int64_t>(tw) * 2 * 148 * 32) tw >>= 1;
+  return tw;
+}
 
 // Validates colind on the device; returns the error bits via *err_host (sync).
 gespmm_status_t device_validate_colind(const int* colind, int64_t nnz, int64_t K,
@@ -278,7 +295,9 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
   }
   size_t tb = tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, tb, packed, E, M32, s);
-  k_count<<<blocks, 256, 0, s>>>(packed, E, M32, cnt);
+  const int tw = tile_work_for(M, plan->nnz);
+  plan->tile_work = tw;
+  k_count<<<blocks, 256, 0, s>>>(packed, E, M32, tw, cnt);
   tb = tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pos, M32, s);
   k_totals<<<1, 1, 0, s>>>(packed, E, cnt, pos, M32, err, tot);
@@ -311,7 +330,7 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
     plan->items_cap = cap;
   }
   tr.mark("totals D2H + items alloc", s);
-  k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, plan->items);
+  k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, tw, plan->items);
   ce = cudaGetLastError();
   cudaFreeAsync(arena, s);
   tr.mark("emit", s);

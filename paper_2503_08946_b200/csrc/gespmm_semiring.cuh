@@ -112,7 +112,11 @@ struct Semiring<GESPMM_REDUCE_MEAN> {
     return __fadd_rn(acc, part);
   }
   __device__ __forceinline__ static float finalize(float acc, int deg, bool accumulate, float c0) {
+#ifdef GESPMM_ABL_MEANMUL  // ablation builds only: the division's cost
+    float r = deg ? acc * static_cast<float>(deg) : 0.0f;
+#else
     float r = deg ? __fdiv_rn(acc, static_cast<float>(deg)) : 0.0f;
+#endif
     return accumulate ? __fadd_rn(c0, r) : r;
   }
 };

@@ -310,6 +310,12 @@ def set_schedule_override(mode: int = -1) -> None:
     _lib.check(_L.gespmm_set_schedule_override(int(mode)))
 
 
+def set_tile_work_override(units: int = 0) -> None:
+    """Tile size (work units) of plans built afterwards: 0 = automatic; results
+    never depend on it.  Test/tuning knob (gespmm_set_tile_work_override)."""
+    _lib.check(_L.gespmm_set_tile_work_override(int(units)))
+
+
 def set_panel_override(cols: int = -1) -> None:
     """Column-panel width: -1 heuristic, 0 never split, > 0 forced width."""
     _lib.check(_L.gespmm_set_panel_override(int(cols)))

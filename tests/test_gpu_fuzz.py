@@ -63,6 +63,8 @@ def test_fuzz_bit_exact(cuda, oracle_mod, case):
     spmm.set_variant_override(variant)
     spmm.set_schedule_override(int(rng.integers(-1, 2)))
     spmm.set_panel_override(int(rng.choice([-1, -1, 0, 32, 64])))
+    tw = int(rng.choice([0, 0, 2, 13, 32, 256]))
+    spmm.set_tile_work_override(tw)
     try:
         plan = Plan(rp, ci, K)
         plan.execute(vv, Bt, op, out=Ct, accumulate=accumulate)
@@ -71,9 +73,10 @@ def test_fuzz_bit_exact(cuda, oracle_mod, case):
         spmm.set_variant_override("")
         spmm.set_schedule_override(-1)
         spmm.set_panel_override(-1)
+        spmm.set_tile_work_override(0)
     want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=accumulate, C0=C0, seg_len=SEG)
     got = Ct.cpu().numpy()
-    np.testing.assert_array_equal(got, want, err_msg=f"case {case}: M={M} K={K} N={N} op={op} variant={variant}")
+    np.testing.assert_array_equal(got, want, err_msg=f"case {case}: M={M} K={K} N={N} op={op} variant={variant} tw={tw}")
     # nothing outside the C view was written
     full = Cbig.cpu().numpy()
     mask = np.ones(full.size, bool)

@@ -165,9 +165,12 @@ def test_column_panels_bit_exact(cuda, oracle_mod, op, N, panel):
         got_acc, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG))
 
 
+@pytest.mark.parametrize("tile_work", [0, 256])
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("op", ["sum", "max", "min"])
-def test_every_variant_bit_exact(cuda, oracle_mod, variant, op):
+def test_every_variant_bit_exact(cuda, oracle_mod, variant, op, tile_work):
+    """Every kernel variant, at the automatic tile size (small here) and the
+    largest (up to 128 rows per tile)."""
     from paper_2503_08946_b200 import spmm
 
     rng = np.random.default_rng(11)
@@ -175,10 +178,14 @@ def test_every_variant_bit_exact(cuda, oracle_mod, variant, op):
     rowptr, colind, vals = random_csr(rng, M, K, 0.04, long_rows=[(10, 3000)], empty_frac=0.4)
     B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
     spmm.set_variant_override(variant)
+    spmm.set_tile_work_override(tile_work)
     try:
-        got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        got, plan = gpu_spmm(cuda, rowptr, colind, vals, B, op)
+        if tile_work:
+            assert plan.info()["tile_work"] == tile_work
     finally:
         spmm.set_variant_override("")
+        spmm.set_tile_work_override(0)
     want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
     np.testing.assert_array_equal(got, want)
 
@@ -234,6 +241,30 @@ def test_max_min_maximum_number_all_bits(cuda, oracle_mod, N, accumulate):
         got, _ = gpu_spmm(cuda, rowptr, colind, vals, B, op, C0=C0)
         want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=accumulate, C0=C0, seg_len=SEG)
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_tile_work_is_automatic_and_result_free(cuda, oracle_mod):
+    """Small matrices get small tiles (more items than warp slots), large ones
+    256; every tile size gives the same bits."""
+    from paper_2503_08946_b200 import spmm
+
+    rng = np.random.default_rng(21)
+    rowptr, colind, vals = random_csr(rng, 3000, 800, 0.02, long_rows=[(5, 900)], empty_frac=0.3)
+    B = rng.uniform(-1, 1, (800, 48)).astype(np.float32)
+    want = oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG)
+    got, plan = gpu_spmm(cuda, rowptr, colind, vals, B, "sum")
+    assert plan.info()["tile_work"] == 16
+    np.testing.assert_array_equal(got, want)
+    for tw in (2, 5, 64, 200, 256):
+        spmm.set_tile_work_override(tw)
+        try:
+            got, plan = gpu_spmm(cuda, rowptr, colind, vals, B, "sum")
+        finally:
+            spmm.set_tile_work_override(0)
+        assert plan.info()["tile_work"] == tw
+        np.testing.assert_array_equal(got, want)
+    with pytest.raises(Exception):
+        spmm.set_tile_work_override(300)
 
 
 def test_segmented_max_equals_unsegmented(cuda, oracle_mod):
