@@ -63,6 +63,10 @@ def parse_args():
                     help="soak length of the extra 'sustained' leg (0 = skip)")
     ap.add_argument("--variant", default="", help="kernel variant override (testing), e.g. vec1_lpr32_cwm2")
     ap.add_argument("--tile-work", type=int, default=0, help="plan tile size override (tuning); 0 = automatic")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = every rank owns one copy of the workload's rows (the job is N "
+                         "row-stacked copies sharing B: per-GPU work fixed); strong = the workload's "
+                         "rows split across ranks (nnz-balanced)")
     ap.add_argument("--ref-sample-products", type=int, default=800_000,
                     help="--impl reference: nnz*N products per step (bounds interpreter RAM)")
     return ap.parse_args()
@@ -449,7 +453,25 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     # ---- row-block sharding (world > 1) ----------------------------------
-    if world > 1:
+    # weak: the job is `world` row-stacked copies of the workload's rows, all
+    # gathering from one B (A_job = [A; A; ...], C_job = [C; C; ...]); rank r
+    # owns rows [r*M, (r+1)*M) -- per-GPU work equals the 1-GPU run.
+    # strong: the workload's own rows split nnz-balanced across ranks.
+    if world > 1 and args.scaling == "weak":
+        bounds = np.arange(world + 1, dtype=np.int64) * M_all
+        rowptr, colind, vals = csr.rowptr, csr.colind, csr.vals
+        M_all, nnz_all = M_all * world, nnz_all * world
+        if rank != 0:
+            B.zero_()  # only the root holds B; the broadcast is the exchange step
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dist.broadcast(B, src=0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bcast_ms = e0.elapsed_time(e1)
+    elif world > 1:
         rp_h = csr.rowptr.cpu().numpy()
         bounds = partition_rows(rp_h, world)
         a, b = int(bounds[rank]), int(bounds[rank + 1])
@@ -643,10 +665,13 @@ def main():
             "metric": "SpMM GFLOP/s (2*nnz*N)",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_job, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic" + (f" ({world} row-stacked copies of the workload sharing B, one per rank)"
+                                   if world > 1 and args.scaling == "weak" else ""),
             "config": {"workload": spec["desc"], "op": args.op, "N": N, "M": M_all, "K": K,
                        "nnz": nnz_all, "l2_flush": f"{flush.numel() * 4 >> 20} MiB written between timed steps",
-                       "parallelism": f"row-block x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"row-block x{world} ({args.scaling} scaling)" if world > 1
+                                       else "single GPU"),
                        "plan": {"n_items": info["n_items"], "n_long_rows": info["n_long_rows"],
                                 "n_segments": info["n_segments"], "build_ms": plan_ms,
                                 "build_wall_ms": plan_wall_ms},

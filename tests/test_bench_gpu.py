@@ -54,3 +54,35 @@ def test_smoke_entry_point():
     import __graft_entry__ as g
 
     g.smoke()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_two_ranks(scaling):
+    """bench.py's N > 1 path, launched as the driver does (torch.distributed.run,
+    127.0.0.1), with two ranks sharing the one GPU over gloo: sharding, the B
+    broadcast, max-over-ranks timing, the fused peer-store C all-gather (CUDA
+    IPC between the two processes) vs the NCCL-style broadcasts, e2e."""
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, GESPMM_BENCH_BACKEND="gloo", GESPMM_NO_PROBE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", "config1",
+                        "--scaling", scaling, "--no-cpu-baseline", "--sustained-s", "0", "--no-clocks"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # rank 0 alone prints
+    d = json.loads(lines[0])
+    one = run_bench("--workload", "config1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+                    "--no-e2e", "--sustained-s", "0", "--no-clocks")
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["value"] > 0
+    assert d["config"]["nnz"] == (2 if scaling == "weak" else 1) * one["config"]["nnz"]
+    ca = d["c_allgather"]
+    assert "error" not in ca, ca
+    assert ca["identical"] is True and ca["fused_peer_stores_ms"] > 0 and ca["nccl_broadcasts_ms"] > 0
+    assert d["e2e"]["value"] > 0 and d["config"]["b_broadcast_ms"] >= 0
