@@ -125,11 +125,25 @@ __device__ __forceinline__ void gather_off(float* d, const float* base, uint32_t
 #ifndef GESPMM_BHINT
 #define GESPMM_BHINT 1  // measured: +1.7% on config 2
 #endif
+// GESPMM_L1EV: L1 eviction priority of the B gathers (0 default allocate,
+// 1 L1::no_allocate, 2 L1::evict_last, 3 L1::evict_first)
+#ifndef GESPMM_L1EV
+#define GESPMM_L1EV 0
+#endif
+#if GESPMM_L1EV == 1
+#define GESPMM_L1Q ".L1::no_allocate"
+#elif GESPMM_L1EV == 2
+#define GESPMM_L1Q ".L1::evict_last"
+#elif GESPMM_L1EV == 3
+#define GESPMM_L1Q ".L1::evict_first"
+#else
+#define GESPMM_L1Q ""
+#endif
 #if GESPMM_BHINT
-#define GESPMM_LDNC "ld.global.nc.L2::cache_hint"
+#define GESPMM_LDNC "ld.global.nc" GESPMM_L1Q ".L2::cache_hint"
 #define GESPMM_POL(n) ", %" #n
 #else
-#define GESPMM_LDNC "ld.global.nc"
+#define GESPMM_LDNC "ld.global.nc" GESPMM_L1Q
 #define GESPMM_POL(n) ""
 #endif
 // address = base + 4 * off in one mad.wide.u32 (ptxas: LEA + LEA.HI.X; the
