@@ -20,7 +20,10 @@ constexpr int kSeg = GESPMM_SEGMENT_LEN;
 // from (nnz, M) alone (never the device): the largest one that still gives
 // every warp slot of a 148-SM B200 (x2) an item, so small matrices are not
 // latency-bound on a few long warps (tile_work_for).
-constexpr int kTileWork = 256;
+#ifndef GESPMM_TILE_MAX
+#define GESPMM_TILE_MAX 256
+#endif
+constexpr int kTileWork = GESPMM_TILE_MAX;
 constexpr int kMinTileWork = 16;
 constexpr int kRowCost = 2;
 // Rows per tile are bounded: every short row advances the work prefix by >= kRowCost.
@@ -33,7 +36,10 @@ constexpr int kWarpsPerBlock = 8;
 // 576: 8 warps x 576 x 8 B = 36.9 KB per CTA, so three CTAs fit per SM next
 // to the gather ring (8 x 4 KB); the bound below covers the 4-alignment of the
 // stage start and the rounding of its end up to a batch of 8.
-constexpr int kStageCap = 576;
+#ifndef GESPMM_STAGE_CAP
+#define GESPMM_STAGE_CAP 576
+#endif
+constexpr int kStageCap = GESPMM_STAGE_CAP;
 static_assert(kTileWork + kSeg + kRowCost + 2 + 3 + 8 <= kStageCap, "stage too small for the largest item");
 // Low 40 bits of the packed plan scan carry tile work, high 24 bits segment counts.
 constexpr int kPackShift = 40;
