@@ -112,8 +112,13 @@ gespmm_status_t gespmm_validate_csr_device(int64_t M, int64_t K, int64_t nnz,
 /* One-shot SpMM on device buffers: C = A (op) B, or C = C0 (op-combine) A (op) B
  * when accumulate != 0 (the reference kernel's C read-modify-write,
  * gespmm_alg2.mir:55-59).  Validates the CSR on the device (the reference
- * validates inside run(), src/oracle.cpp:700), builds a temporary plan,
- * launches, and releases the plan stream-ordered.  Synchronizes once (plan). */
+ * validates inside run(), src/oracle.cpp:700), re-plans a cached per-device
+ * plan in place (no allocation per call: cudaFree would synchronize the
+ * device), launches, and returns after the launches complete -- it
+ * synchronizes `stream` twice (the plan's totals, the end of the call; calls
+ * are serialized by a process-wide lock).  For asynchronous repeated
+ * execution build a plan once (gespmm_plan_create) and use
+ * gespmm_plan_execute, which never synchronizes. */
 gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
                                 const int32_t* rowptr, const int32_t* colind,
                                 const float* vals, const float* B, int64_t ldb, float* C,
@@ -138,7 +143,10 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
 gespmm_status_t gespmm_plan_create(gespmm_plan_t* plan, int64_t M, int64_t K, int64_t nnz,
                                    const int32_t* rowptr, const int32_t* colind, int flags,
                                    void* stream);
-/* Launch with a plan (asynchronous on `stream`, no host synchronization). */
+/* Launch with a plan (asynchronous on `stream`, no host synchronization once
+ * the plan's workspace -- long-row partials and counters, sized by N -- has
+ * been allocated; growing it, on the first call or a wider N, uses
+ * cudaMalloc/cudaFree, which may synchronize the device). */
 gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t* rowptr,
                                     const int32_t* colind, const float* vals, const float* B,
                                     int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
