@@ -652,8 +652,9 @@ def main():
                "d2h_bytes_per_step": int(4 * M_loc * N),
                "ms_per_step": float(e2e_t.item()) * 1e3,
                "path": "gespmm_csr_spmm_host (pinned host buffers; pipelined: rowptr + B H2D, "
-                       "plan, then per row chunk colind/vals H2D -> device colind check -> kernel "
-                       "-> C rows D2H overlapping the next chunk; wall clock per call)"}
+                       "plan, then per item-aligned row chunk, fewest nonzeros first: colind/vals "
+                       "H2D -> device colind check -> kernel -> C rows D2H overlapping the next "
+                       "chunk; wall clock per call)"}
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
     cpu = None

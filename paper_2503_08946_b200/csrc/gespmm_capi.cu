@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -26,6 +27,8 @@ cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc,
                          cudaStream_t s);
 cudaError_t row_item_range(const gespmm_plan_s* plan, const int64_t* rows, int64_t* d_range,
                            cudaStream_t s);
+cudaError_t chunk_rows_aligned(const gespmm_plan_s* plan, const int64_t* rows, int nc, int64_t* d_ranges,
+                               int64_t* d_rows, cudaStream_t s);
 cudaError_t validate_colind_async(const int* colind, int64_t p0, int64_t p1, int64_t K, int* err,
                                   cudaStream_t s);
 std::string csr_error_message(int err, int64_t K);
@@ -45,10 +48,12 @@ static double now_ms() {
 }
 
 // GESPMM_TRACE=1: synchronize at each mark (device phase times);
-// GESPMM_TRACE=2: host timestamps only (where the host thread blocks).
+// GESPMM_TRACE=2: host timestamps only (where the host thread blocks);
+// GESPMM_TRACE=3: no marks; the pipelined host entry prints its device
+// timeline (per-chunk copy / launch completion events, no added syncs).
 Trace::Trace(const char* s) : scope(s) {
   const char* e = std::getenv("GESPMM_TRACE");
-  on = e && *e && *e != '0';
+  on = e && *e && *e != '0' && *e != '3';
   sync = on && *e != '2';
   if (on) t0 = last = now_ms();
 }
@@ -567,7 +572,7 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   Trace tr("host");
   auto al = [](int64_t bytes) { return (bytes + 255) & ~int64_t(255); };
   const int64_t b_rp = al((M + 1) * 4), b_ci = al(nnz * 4), b_v = al(nnz * 4),
-                b_B = al(K * N * 4), b_C = al(M * N * 4), b_x = al(8 * (kMaxChunks + 1) + 64);
+                b_B = al(K * N * 4), b_C = al(M * N * 4), b_x = al(16 * (kMaxChunks + 1) + 64);
   char* ws = nullptr;
   st = host_workspace(b_rp + b_ci + b_v + b_B + b_C + b_x, &ws);
   if (st != GESPMM_OK) return st;
@@ -577,50 +582,48 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   auto* d_B = reinterpret_cast<float*>(ws + b_rp + b_ci + b_v);
   auto* d_C = reinterpret_cast<float*>(ws + b_rp + b_ci + b_v + b_B);
   auto* d_ranges = reinterpret_cast<int64_t*>(ws + b_rp + b_ci + b_v + b_B + b_C);
-  auto* d_err = reinterpret_cast<int*>(d_ranges + kMaxChunks + 1);
+  auto* d_rows = d_ranges + kMaxChunks + 1;
+  auto* d_err = reinterpret_cast<int*>(d_rows + kMaxChunks + 1);
   Pipe* pp = nullptr;
   st = pipe_streams(&pp);
   if (st != GESPMM_OK) return st;
   cudaStream_t s_in = pp->in, s_out = pp->out;
   tr.mark("workspace", s);
 
-  // Row chunks: contiguous rows with ~equal nnz + rows; C rows of chunk c go
-  // back to the host as soon as chunk c's launch is done, while chunk c+1's
-  // colind/vals are still arriving (PCIe is full duplex).  Chunks need >= ~8 MB
-  // of C each to amortize their launches and copies.
+  // Row chunks of ~equal rows (= equal C bytes, equal D2H time), their
+  // boundaries moved to item starts so every chunk's launch writes exactly
+  // its own C rows (no tile spans two chunks); processed in order of
+  // increasing nonzeros: C rows that need the least colind/vals go back to
+  // the host first, so the D2H stream starts right after B arrives and the
+  // heavy chunks' H2D overlaps the C drain (PCIe is full duplex).  R-MAT puts
+  // a third of the nonzeros in the first 1/16 of the rows; in row order the
+  // D2H stream idled behind them (11.3 ms).
   const int64_t c_bytes = M * N * 4;
   int nc = static_cast<int>(c_bytes / (8 << 20));
   if (nc > kMaxChunks) nc = kMaxChunks;
   if (nc < 1 || std::getenv("GESPMM_HOST_NO_PIPELINE")) nc = 1;
-  int64_t rows[kMaxChunks + 1];
-  rows[0] = 0;
-  rows[nc] = M;
-  for (int c = 1; c < nc; ++c) {  // first row whose (nnz + rows) prefix reaches c/nc of the total
-    const double target = static_cast<double>(nnz + M) * c / nc;
-    int64_t lo = rows[c - 1], hi = M;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (static_cast<double>(rowptr[mid]) + static_cast<double>(mid) < target) lo = mid + 1;
-      else hi = mid;
-    }
-    rows[c] = lo;
-  }
-  // A launch over chunk c's items can read up to kStageCap + 4 nonzeros past
-  // rowptr[rows[c+1]] (a tile that starts in chunk c and runs into chunk c+1,
-  // plus the 16-byte staging granule): chunk c's transfer covers that overhang.
-  const int64_t overhang = kStageCap + 4;
-  auto pos_end = [&](int c) {
-    const int64_t p = static_cast<int64_t>(rowptr[rows[c + 1]]) + (c + 1 < nc ? overhang : 0);
-    return p < nnz ? p : nnz;
-  };
+  const bool in_row_order = std::getenv("GESPMM_HOST_ROW_ORDER") != nullptr;  // A/B switch
+  // A launch reads its item's colind/vals up to the 16-byte staging granule
+  // past the item end (never folded); chunk transfers cover that overhang.
+  const int64_t overhang = 16;
 
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t x) {
     if (e == cudaSuccess) e = x;
   };
-  // ---- host -> device on s_in: rowptr, B (and C0), then colind/vals per chunk
+  // GESPMM_TRACE=3: device timeline of this call (timing events, no syncs)
+  const char* trace_env = std::getenv("GESPMM_TRACE");
+  const bool tl = trace_env && *trace_env == '3';
+  cudaEvent_t tev[3 + 3 * kMaxChunks] = {};
+  auto tmark = [&](int i, cudaStream_t st) {
+    if (!tl) return;
+    if (!tev[i]) cudaEventCreate(&tev[i]);
+    cudaEventRecord(tev[i], st);
+  };
+  // ---- host -> device on s_in: rowptr, B (and C0) ----------------------------
   chk(cudaEventRecord(pp->ev[0], s));  // s_in must not overtake prior work on s
   chk(cudaStreamWaitEvent(s_in, pp->ev[0], 0));
+  tmark(0, s_in);
   chk(cudaMemcpyAsync(d_rp, rowptr, static_cast<size_t>(M + 1) * 4, cudaMemcpyHostToDevice, s_in));
   chk(cudaEventRecord(pp->ev[1], s_in));  // rowptr resident
   if (K > 0) {
@@ -631,24 +634,13 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
     if (ldc == N) chk(cudaMemcpyAsync(d_C, C, static_cast<size_t>(M * N) * 4, cudaMemcpyHostToDevice, s_in));
     else chk(cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s_in));
   }
-  int64_t sent = 0;
-  for (int c = 0; c < nc; ++c) {
-    const int64_t p1 = pos_end(c);
-    if (p1 > sent) {
-      chk(cudaMemcpyAsync(d_ci + sent, colind + sent, static_cast<size_t>(p1 - sent) * 4,
-                          cudaMemcpyHostToDevice, s_in));
-      chk(cudaMemcpyAsync(d_v + sent, vals + sent, static_cast<size_t>(p1 - sent) * 4,
-                          cudaMemcpyHostToDevice, s_in));
-      sent = p1;
-    }
-    chk(cudaEventRecord(pp->ev[2 + c], s_in));  // chunk c's nonzeros resident
-  }
+  tmark(1, s_in);  // rowptr + B (+ C0) resident
   if (e != cudaSuccess) {
     cudaStreamSynchronize(s_in);
     return cuda_fail(e, "host to device copy");
   }
   tr.mark("H2D issued", s);
-  // ---- plan from rowptr (overlaps the B transfer), chunk item ranges --------
+  // ---- plan from rowptr (overlaps the B transfer), item-aligned chunks -------
   chk(cudaStreamWaitEvent(s, pp->ev[1], 0));
   chk(cudaMemsetAsync(d_err, 0, sizeof(int), s));
   // The plan object is cached per device with the workspace and re-planned in
@@ -663,19 +655,42 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
     cudaStreamSynchronize(s_in);
     return e != cudaSuccess ? cuda_fail(e, "plan") : st;
   }
-  chk(chunk_ranges(plan, rows, nc, d_ranges, s));
+  int64_t rows[kMaxChunks + 1];
+  for (int c = 0; c <= nc; ++c) rows[c] = M * c / nc;
+  chk(chunk_rows_aligned(plan, rows, nc, d_ranges, d_rows, s));
+  chk(cudaMemcpyAsync(rows, d_rows, static_cast<size_t>(nc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  chk(cudaStreamSynchronize(s));  // ~20 us; B is still in flight
+  int order[kMaxChunks];
+  for (int c = 0; c < nc; ++c) order[c] = c;
+  auto nnz_of = [&](int c) { return static_cast<int64_t>(rowptr[rows[c + 1]]) - rowptr[rows[c]]; };
+  if (!in_row_order)
+    std::stable_sort(order, order + nc, [&](int a, int b) { return nnz_of(a) < nnz_of(b); });
+  // ---- colind/vals per chunk, in processing order, behind B on s_in ----------
+  for (int k = 0; k < nc && e == cudaSuccess; ++k) {
+    const int c = order[k];
+    const int64_t p0 = rowptr[rows[c]];
+    int64_t p1 = static_cast<int64_t>(rowptr[rows[c + 1]]) + overhang;
+    if (p1 > nnz) p1 = nnz;
+    if (p1 > p0) {
+      chk(cudaMemcpyAsync(d_ci + p0, colind + p0, static_cast<size_t>(p1 - p0) * 4, cudaMemcpyHostToDevice, s_in));
+      chk(cudaMemcpyAsync(d_v + p0, vals + p0, static_cast<size_t>(p1 - p0) * 4, cudaMemcpyHostToDevice, s_in));
+    }
+    chk(cudaEventRecord(pp->ev[2 + k], s_in));  // chunk c's nonzeros resident
+    tmark(3 + k, s_in);
+  }
   tr.mark("rowptr H2D + plan", s);
   // ---- per chunk: colind check, the launch(es), C rows back on s_out --------
-  for (int c = 0; c < nc && e == cudaSuccess; ++c) {
-    const int64_t p0 = c == 0 ? 0 : pos_end(c - 1);
-    chk(cudaStreamWaitEvent(s, pp->ev[2 + c], 0));
-    chk(validate_colind_async(d_ci, p0, pos_end(c), K, d_err, s));
+  for (int k = 0; k < nc && e == cudaSuccess; ++k) {
+    const int c = order[k];
+    chk(cudaStreamWaitEvent(s, pp->ev[2 + k], 0));
+    chk(validate_colind_async(d_ci, rowptr[rows[c]], rowptr[rows[c + 1]], K, d_err, s));
     if (e != cudaSuccess) break;
     st = execute_range(plan, N, d_rp, d_ci, d_v, d_B, N, d_C, N, op, accumulate,
                        nc > 1 ? d_ranges + c : nullptr, d_err, s);
     if (st != GESPMM_OK) break;
-    chk(cudaEventRecord(pp->ev[2 + kMaxChunks + c], s));
-    chk(cudaStreamWaitEvent(s_out, pp->ev[2 + kMaxChunks + c], 0));
+    chk(cudaEventRecord(pp->ev[2 + kMaxChunks + k], s));
+    tmark(3 + kMaxChunks + k, s);
+    chk(cudaStreamWaitEvent(s_out, pp->ev[2 + kMaxChunks + k], 0));
     const int64_t r0 = rows[c], nr = rows[c + 1] - rows[c];
     if (nr > 0) {
       if (ldc == N)
@@ -685,7 +700,9 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
         chk(cudaMemcpy2DAsync(C + r0 * ldc, ldc * 4, d_C + r0 * N, N * 4, N * 4, nr,
                               cudaMemcpyDeviceToHost, s_out));
     }
+    tmark(3 + 2 * kMaxChunks + k, s_out);
   }
+  tmark(2, s);  // plan + all launches done (s)
   tr.mark("chunks issued", s);
   int h_err = 0;
   chk(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -697,6 +714,22 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   chk(e2);
   chk(e3);
   tr.mark("chunks + C D2H", s);
+  if (tl) {  // ms from the first copy: inputs resident / chunk c H2D, launch, D2H done
+    auto at = [&](int i) {
+      float ms = -1.f;
+      if (tev[i] && tev[0]) cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      return ms;
+    };
+    std::fprintf(stderr, "[gespmm timeline] rowptr+B resident %.3f ms, %d chunks\n", at(1), nc);
+    for (int k = 0; k < nc; ++k) {
+      const int c = order[k];
+      std::fprintf(stderr, "[gespmm timeline] chunk %2d rows %9lld nnz %10lld: H2D %.3f  kernel %.3f  D2H %.3f\n",
+                   c, static_cast<long long>(rows[c + 1] - rows[c]), static_cast<long long>(nnz_of(c)),
+                   at(3 + k), at(3 + kMaxChunks + k), at(3 + 2 * kMaxChunks + k));
+    }
+    for (cudaEvent_t x : tev)
+      if (x) cudaEventDestroy(x);
+  }
   if (st != GESPMM_OK) return st;
   if (e != cudaSuccess) return cuda_fail(e, "pipelined host spmm");
   // C's contents are unspecified after CSR_INVALID (earlier chunks may have

@@ -145,7 +145,40 @@ __global__ void k_chunk_ranges(const int4* __restrict__ items, int64_t n_items, 
   ranges[c] = (pin && c == 0) ? 0 : lo;
 }
 
+// Item-aligned chunk rows: out_rows[c] = the first row of the first item whose
+// row is >= rows.r[c] (so no tile spans two chunks), out_rows[nc] = M, and
+// ranges[c] = that item (ranges[nc] = n_items).
+__global__ void k_chunk_rows_aligned(const int4* __restrict__ items, int64_t n_items, int64_t M,
+                                     ChunkRows rows, int nc, int64_t* __restrict__ ranges,
+                                     int64_t* __restrict__ out_rows) {
+  const int c = threadIdx.x;
+  if (c > nc) return;
+  if (c == nc) {
+    ranges[c] = n_items;
+    out_rows[c] = M;
+    return;
+  }
+  int64_t lo = 0, hi = n_items;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (items[mid].x < rows.r[c]) lo = mid + 1;
+    else hi = mid;
+  }
+  if (c == 0) lo = 0;
+  ranges[c] = lo;
+  out_rows[c] = c == 0 ? 0 : (lo < n_items ? static_cast<int64_t>(items[lo].x) : M);
+}
+
 }  // namespace
+
+cudaError_t chunk_rows_aligned(const gespmm_plan_s* plan, const int64_t* rows, int nc, int64_t* d_ranges,
+                               int64_t* d_rows, cudaStream_t s) {
+  if (nc < 1 || nc > kMaxChunks) return cudaErrorInvalidValue;
+  ChunkRows cr{};
+  for (int c = 0; c <= nc; ++c) cr.r[c] = rows[c];
+  k_chunk_rows_aligned<<<1, 32, 0, s>>>(plan->items, plan->n_items, plan->M, cr, nc, d_ranges, d_rows);
+  return cudaGetLastError();
+}
 
 cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc, int64_t* d_ranges,
                          cudaStream_t s) {
