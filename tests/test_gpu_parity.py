@@ -442,6 +442,38 @@ def test_host_entry_point_pipelined_invalid_colind(cuda, oracle_mod):
     np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG))
 
 
+@pytest.mark.parametrize("op", ["sum", "min"])
+def test_host_entry_point_front_loaded_chunks(cuda, oracle_mod, op):
+    """Nonzeros piled into the first rows (as in R-MAT): the host pipeline runs
+    its item-aligned chunks out of row order (fewest nonzeros first); results
+    bit-exact, with and without accumulate, and an invalid column in the chunk
+    that runs first or last is reported the same way."""
+    from paper_2503_08946_b200.errors import Error, ErrorKind
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    rng = np.random.default_rng(42)
+    M, K, N = 150_000, 30_000, 64
+    deg = np.where(np.arange(M) < M // 10, rng.integers(50, 400, M), rng.integers(0, 4, M))
+    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    colind = rng.integers(0, K, int(rowptr[-1])).astype(np.int32)
+    vals = rng.uniform(-1, 1, colind.size).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, op)
+    np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, op, C0=C0)
+    np.testing.assert_array_equal(
+        got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG))
+    for pos in (int(rowptr[M // 20]), int(rowptr[-1]) - 3):  # heavy chunk (runs last) / light one (first)
+        bad = colind.copy()
+        bad[pos] = -7
+        with pytest.raises(Error) as ei:
+            csr_spmm_host(rowptr, bad, vals, B, op)
+        assert ei.value.kind == ErrorKind.CsrInvalid
+    got = csr_spmm_host(rowptr, colind, vals, B, op)
+    np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+
+
 def test_deterministic_and_shard_invariant(cuda, oracle_mod):
     """Same bits run-to-run, and row-sharded computation (the multi-GPU path's
     per-rank work) reproduces the unsharded result bit for bit."""
