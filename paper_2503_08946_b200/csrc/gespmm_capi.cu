@@ -630,11 +630,7 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
     if (ldb == N) chk(cudaMemcpyAsync(d_B, B, static_cast<size_t>(K * N) * 4, cudaMemcpyHostToDevice, s_in));
     else chk(cudaMemcpy2DAsync(d_B, N * 4, B, ldb * 4, N * 4, K, cudaMemcpyHostToDevice, s_in));
   }
-  if (accumulate) {
-    if (ldc == N) chk(cudaMemcpyAsync(d_C, C, static_cast<size_t>(M * N) * 4, cudaMemcpyHostToDevice, s_in));
-    else chk(cudaMemcpy2DAsync(d_C, N * 4, C, ldc * 4, N * 4, M, cudaMemcpyHostToDevice, s_in));
-  }
-  tmark(1, s_in);  // rowptr + B (+ C0) resident
+  tmark(1, s_in);  // rowptr + B resident
   if (e != cudaSuccess) {
     cudaStreamSynchronize(s_in);
     return cuda_fail(e, "host to device copy");
@@ -674,6 +670,13 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
     if (p1 > p0) {
       chk(cudaMemcpyAsync(d_ci + p0, colind + p0, static_cast<size_t>(p1 - p0) * 4, cudaMemcpyHostToDevice, s_in));
       chk(cudaMemcpyAsync(d_v + p0, vals + p0, static_cast<size_t>(p1 - p0) * 4, cudaMemcpyHostToDevice, s_in));
+    }
+    const int64_t r0 = rows[c], nr = rows[c + 1] - rows[c];
+    if (accumulate && nr > 0) {  // C0 rows of this chunk (its launch touches only these)
+      if (ldc == N)
+        chk(cudaMemcpyAsync(d_C + r0 * N, C + r0 * N, static_cast<size_t>(nr * N) * 4, cudaMemcpyHostToDevice, s_in));
+      else
+        chk(cudaMemcpy2DAsync(d_C + r0 * N, N * 4, C + r0 * ldc, ldc * 4, N * 4, nr, cudaMemcpyHostToDevice, s_in));
     }
     chk(cudaEventRecord(pp->ev[2 + k], s_in));  // chunk c's nonzeros resident
     tmark(3 + k, s_in);
