@@ -2,6 +2,8 @@
 rows, empty rows, duplicate/unsorted columns, odd N, strided/misaligned B and
 C, accumulate, every reduce op, both item schedules, forced column panels and
 forced kernel variants -- GPU bit-exact to the fp32 twin in every case."""
+import os
+
 import numpy as np
 import pytest
 
@@ -24,7 +26,7 @@ def rand_csr(rng, M, K, mean_deg):
     return rowptr, colind, vals
 
 
-CASES = list(range(200))
+CASES = list(range(int(os.environ.get("GESPMM_FUZZ_CASES", "200"))))
 
 
 @pytest.mark.gpu
@@ -42,6 +44,12 @@ def test_fuzz_bit_exact(cuda, oracle_mod, case):
     op = ["sum", "max", "min", "mean"][case % 4]
     rowptr, colind, vals = rand_csr(rng, M, K, float(rng.uniform(1, 40)))
     B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    special = rng.random() < 0.15  # NaN / inf / -0 operands
+    if special and vals.size:
+        vals[rng.integers(0, vals.size, max(1, vals.size // 40))] = np.nan
+        vals[rng.integers(0, vals.size, max(1, vals.size // 40))] = -0.0
+        B.ravel()[rng.integers(0, B.size, max(1, B.size // 30))] = np.inf
+        B.ravel()[rng.integers(0, B.size, max(1, B.size // 30))] = -0.0
     accumulate = rng.random() < 0.3
     C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32) if accumulate else None
     # strided / offset views of B and C
@@ -77,6 +85,8 @@ def test_fuzz_bit_exact(cuda, oracle_mod, case):
     want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=accumulate, C0=C0, seg_len=SEG)
     got = Ct.cpu().numpy()
     np.testing.assert_array_equal(got, want, err_msg=f"case {case}: M={M} K={K} N={N} op={op} variant={variant} tw={tw}")
+    if op in ("max", "min"):  # maximumNumber: every bit, NaNs included
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=f"case {case} bits")
     # nothing outside the C view was written
     full = Cbig.cpu().numpy()
     mask = np.ones(full.size, bool)
