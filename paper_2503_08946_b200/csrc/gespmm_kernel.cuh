@@ -1,9 +1,10 @@
 // gespmm_kernel.cuh -- the B200 GE-SpMM kernel family (sm_100a), instantiated
 // per reduce op in gespmm_spmm_<op>.cu.
 //
-// What it computes: C[i, j] = reduce_{p in row i, ascending} val[p] * B[col[p], j]
+// What it computes: C[i, j] = reduce_{p in row i} val[p] * B[col[p], j]
 // (reference kernel /root/reference/proj/fixtures/gespmm_alg2.mir:21-69;
-// reduce functors in gespmm_semiring.cuh).
+// reduce functors in gespmm_semiring.cuh: sum/mean as two ascending FMA
+// chains, max/min as the order-free maximumNumber/minimumNumber).
 //
 // How:
 //  * One warp per work item.  An item is either a TILE of consecutive short
@@ -12,11 +13,15 @@
 //  * Coalesced Row Caching: the warp copies the item's whole colind/vals span
 //    (<= kStageCap nonzeros) into its slice of shared memory with 16-byte
 //    cp.async per lane (fully coalesced, no register cost, one commit/wait),
-//    plus the tile's rowptr window.  One __syncwarp() publishes the stage --
-//    the warp-scoped form of the reference's staging barrier
-//    (gespmm_alg2.mir:36); another at the top of the next item orders the
-//    stage reads before the refill (the reference's second barrier, mir:65).
-//  * Persistent warps walk the work list with a warp stride; a segment runs
+//    plus the tile's rowptr window; each lane then pre-scales (col -> col*ldb)
+//    and pad-zeroes the entries its own copy delivered.  One __syncwarp()
+//    publishes the stage -- the warp-scoped form of the reference's staging
+//    barrier (gespmm_alg2.mir:36); another at the top of the next item orders
+//    the stage reads before the refill (the reference's second barrier,
+//    mir:65).  Certified by the reference's race checker
+//    (oracle/models/gespmm_b200_stage.model).
+//  * Persistent warps walk the work list (an atomic counter per column block
+//    for large plans, a warp stride for small ones); a segment runs
 //    through the same pipeline as a one-row tile (one code path: the kernel
 //    must stay inside the instruction cache).
 //  * Coarse-grained Warp Merging: each lane owns VEC consecutive columns in each
@@ -27,7 +32,7 @@
 //    registers), then folded; at one column per lane (N <= 32 tiles) runs of
 //    16 in-row positions are gathered at once.  The memory-level parallelism
 //    this buffer allows is the kernel's bound (tools/gather_probe.cu: the
-//    gather-only replay of the same stream at the same MLP takes ~81-85 % of
+//    gather-only replay of the same stream at the same MLP takes ~88 % of
 //    the kernel's time).  TMA gather4 reaches only 3-7 TB/s for 256-byte rows,
 //    so the gathers stay in LDG.  At 512-byte rows (N=128 tiles) the B rows
 //    instead go through a per-warp shared-memory ring with cp.async (Ring<>),
