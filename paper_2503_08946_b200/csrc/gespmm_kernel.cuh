@@ -144,11 +144,23 @@ __device__ __forceinline__ void gather_off(float* d, const float* base, uint32_t
 #else
 #define GESPMM_L1Q ""
 #endif
+// GESPMM_PF: L2 prefetch size qualifier of the B gathers (0 none, 1 .L2::128B,
+// 2 .L2::256B)
+#ifndef GESPMM_PF
+#define GESPMM_PF 0
+#endif
+#if GESPMM_PF == 1
+#define GESPMM_PFQ ".L2::128B"
+#elif GESPMM_PF == 2
+#define GESPMM_PFQ ".L2::256B"
+#else
+#define GESPMM_PFQ ""
+#endif
 #if GESPMM_BHINT
-#define GESPMM_LDNC "ld.global.nc" GESPMM_L1Q ".L2::cache_hint"
+#define GESPMM_LDNC "ld.global.nc" GESPMM_L1Q ".L2::cache_hint" GESPMM_PFQ
 #define GESPMM_POL(n) ", %" #n
 #else
-#define GESPMM_LDNC "ld.global.nc" GESPMM_L1Q
+#define GESPMM_LDNC "ld.global.nc" GESPMM_L1Q GESPMM_PFQ
 #define GESPMM_POL(n) ""
 #endif
 // address = base + 4 * off in one mad.wide.u32 (ptxas: LEA + LEA.HI.X; the
