@@ -56,3 +56,18 @@ def test_cpu_baseline_leg_small():
     r = bench.cpu_baseline_port(c, B, 16, budget_s=0.2)
     assert r["kind"] == "port" and r["cores"] >= 1 and r["value"] > 0
     assert r["single_thread"]["cores"] == 1 and r["single_thread"]["value"] > 0
+
+
+def test_ncu_metrics_file_covers_the_default_line():
+    """roofline.ncu: the committed capture's DRAM throughput and L2 hit rate
+    (report both beside the algorithmic fraction)."""
+    import json
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "profiles", "ncu_metrics.json")) as f:
+        d = json.load(f)
+    m = d["config2:sum"]
+    assert 0 < m["dram_throughput_pct"] < 100 and 0 < m["l2_hit_pct"] < 100
+    with open(os.path.join(root, "profiles", "traffic.json")) as f:
+        assert json.load(f)["config2:sum"] == m["dram_bytes"]
