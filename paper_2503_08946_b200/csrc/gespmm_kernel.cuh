@@ -287,9 +287,19 @@ struct Pipe {
 // Min CTAs per SM for __launch_bounds__: caps registers so 32 warps/SM are
 // resident; with two buffers in flight per warp that is ~128 KB of gathers
 // per SM at N=64 (the L2 gather ceiling needs about that much).
+// 8 columns per lane (N >= 256 tiles): 2 CTAs/SM, 106 registers, no spills
+// (at 3 CTAs/SM the 80-register cap spilled 56-72 bytes: R-MAT 2^22 x N=256
+// 7.29 -> 6.60 ms, 2^20 x 256 1.46 -> 1.32 ms)
+#ifndef GESPMM_MINBLOCKS_WIDE
+#define GESPMM_MINBLOCKS_WIDE 2
+#endif
+#ifndef GESPMM_MINBLOCKS_ONE
+#define GESPMM_MINBLOCKS_ONE GESPMM_MINBLOCKS  // 1 column per lane (N <= 32 tiles)
+#endif
 template <int CPL>
 struct MinBlocks {
-  static constexpr int value = CPL >= 8 ? 3 : GESPMM_MINBLOCKS;
+  static constexpr int value =
+      CPL >= 8 ? GESPMM_MINBLOCKS_WIDE : (CPL == 1 ? GESPMM_MINBLOCKS_ONE : GESPMM_MINBLOCKS);
 };
 
 // Ring mode (RING = true; DESIGN.md 5.2 "Gather ring"): B rows are copied
