@@ -572,21 +572,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       // them for it), so with 16-byte staging no warp barrier is needed before this pass
       // (oracle/models/gespmm_b200_stage.model: copy and pre-scale share a
       // warp phase); the barrier after it publishes the stage.
+      // The head [sbase, lo) -- up to 3 entries of the previous item, which a
+      // chunked launch may not have transferred or validated yet -- is zeroed
+      // the same way: a launch never gathers through an entry outside its
+      // item.
       const uint32_t ldb32 = static_cast<uint32_t>(ldb);
-      const int pad = hi - sbase;
+      const int pad = hi - sbase, head = lo - sbase;
+      auto keep = [&](int j) { return j >= head && j < pad; };
       for (int i = 4 * lane; i < send - sbase; i += 128) {
         int4 c = *reinterpret_cast<int4*>(sc + i);
-        c.x = i + 0 < pad ? static_cast<int>(static_cast<uint32_t>(c.x) * ldb32) : 0;
-        c.y = i + 1 < pad ? static_cast<int>(static_cast<uint32_t>(c.y) * ldb32) : 0;
-        c.z = i + 2 < pad ? static_cast<int>(static_cast<uint32_t>(c.z) * ldb32) : 0;
-        c.w = i + 3 < pad ? static_cast<int>(static_cast<uint32_t>(c.w) * ldb32) : 0;
+        c.x = keep(i + 0) ? static_cast<int>(static_cast<uint32_t>(c.x) * ldb32) : 0;
+        c.y = keep(i + 1) ? static_cast<int>(static_cast<uint32_t>(c.y) * ldb32) : 0;
+        c.z = keep(i + 2) ? static_cast<int>(static_cast<uint32_t>(c.z) * ldb32) : 0;
+        c.w = keep(i + 3) ? static_cast<int>(static_cast<uint32_t>(c.w) * ldb32) : 0;
         *reinterpret_cast<int4*>(sc + i) = c;
       }
       __syncwarp();
     } else {
       __syncwarp();
       // zero the pad [hi, send) (overwrites any neighbours cp.async brought in)
+      // and the head [sbase, lo) (never gather through another item's entry)
       for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;
+      if (lane < lo - sbase) sc[lane] = 0;
       __syncwarp();
       if (OFF32) {  // col -> B-row element offset col*ldb, once per staged entry
         const uint32_t ldb32 = static_cast<uint32_t>(ldb);

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     cp_async_wait_all();
     __syncwarp();
     for (int i = hi - sbase + lane; i < send - sbase; i += 32) sc[i] = 0;  // pad: row 0, never folded
+    if (lane < lo - sbase) sc[lane] = 0;  // head: another item's entries, never gathered through
     __syncwarp();
     {
       const uint32_t ldb32 = static_cast<uint32_t>(ldb);

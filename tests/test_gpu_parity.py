@@ -474,6 +474,34 @@ def test_host_entry_point_front_loaded_chunks(cuda, oracle_mod, op):
     np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
 
 
+def test_host_entry_point_never_gathers_through_stale_entries(cuda, oracle_mod):
+    """Chunks run out of row order, so the 16-byte staging granule before a
+    chunk's first item can hold entries of a chunk not yet transferred (here:
+    stale columns of a previous call with K = 20 M).  The kernel zeroes the
+    staged head before its item: no gather leaves B, results stay exact.
+    (Best effort: a stale gather only faults when it lands on unmapped
+    memory; the build without the head zeroing passed this test too.)"""
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    rng = np.random.default_rng(43)
+    Kbig = 20_000_000
+    rp1 = np.linspace(0, 3_000_000, 4001).astype(np.int32)
+    ci1 = rng.integers(Kbig // 2, Kbig, 3_000_000).astype(np.int32)
+    v1 = np.ones(ci1.size, np.float32)
+    B1 = np.ones((Kbig, 1), np.float32)
+    csr_spmm_host(rp1, ci1, v1, B1, "sum")  # leaves large columns in the workspace
+    M, K, N = 150_000, 30_000, 64
+    deg = np.where(np.arange(M) < M // 10, rng.integers(20, 200, M), rng.integers(0, 3, M))
+    deg[rng.random(M) < 0.3] += 1  # ragged chunk starts (not 4-aligned)
+    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    colind = rng.integers(0, K, int(rowptr[-1])).astype(np.int32)
+    vals = rng.uniform(-1, 1, colind.size).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    for op in ("sum", "max"):
+        got = csr_spmm_host(rowptr, colind, vals, B, op)
+        np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+
+
 def test_deterministic_and_shard_invariant(cuda, oracle_mod):
     """Same bits run-to-run, and row-sharded computation (the multi-GPU path's
     per-rank work) reproduces the unsharded result bit for bit."""
