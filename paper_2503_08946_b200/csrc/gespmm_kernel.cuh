@@ -184,6 +184,11 @@ __device__ __forceinline__ void gather_off<4>(float* d, const float* base, uint3
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
       : "r"(off), "l"(base), "l"(pol));
 }
+// GESPMM_SADDR=1: the batch loop reads the stage through one 32-bit shared
+// address (stage entries and vals at immediate offsets) -- A/B knob
+#ifndef GESPMM_SADDR
+#define GESPMM_SADDR 1  // config 3 N=32: 1.271 -> 1.166 ms; configs 2/3-64 neutral
+#endif
 #ifndef GESPMM_MERGED_PAD
 #define GESPMM_MERGED_PAD 1  // pad zeroing folded into the offset pre-scale pass
 #endif
@@ -339,8 +344,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   using RG = Ring<VEC, CWM>;
   static_assert(!RING || RG::kSupported, "ring mode: CWM == 1, VEC >= 2");
   constexpr int TW = 32 * VEC;         // columns per CWM tile
+#if GESPMM_SADDR
+  // one block per warp: colind slice, then vals slice (a fixed 4*kStageCap-byte
+  // offset the batch loads take as an immediate)
+  __shared__ __align__(16) int stg[kWarpsPerBlock][2 * kStageCap];
+#else
   __shared__ __align__(16) int scol[kWarpsPerBlock][kStageCap];
   __shared__ __align__(16) float sval[kWarpsPerBlock][kStageCap];
+#endif
   __shared__ int rpw[kWarpsPerBlock][kTileMaxRows + 4];
 
   const int warp = threadIdx.x >> 5;
@@ -370,8 +381,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     const int64_t c = static_cast<int64_t>(cb) * TW + 4 * rchunk;
     return P.B + (c < P.N ? c : 0);
   }();
+#if GESPMM_SADDR
+  int* const sc = stg[warp];
+  float* const sv = reinterpret_cast<float*>(stg[warp] + kStageCap);
+#else
   int* const sc = scol[warp];
   float* const sv = sval[warp];
+#endif
   int* const rp = rpw[warp];
   const bool accumulate = P.accumulate != 0;
   const bool seed_c0 = accumulate && SR::kSeedC0;
@@ -640,11 +656,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
+#if GESPMM_SADDR
+    // 32-bit shared address of stage entry 0 relative to position 0
+    const uint32_t s_pos0 = static_cast<uint32_t>(__cvta_generic_to_shared(sc)) - 4u * static_cast<uint32_t>(sbase);
+#endif
     auto issue = [&](int qb, float (&b)[U][CWM][VEC]) {
       const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
 #pragma unroll
       for (int g = 0; g < U / 4; ++g) {
+#if GESPMM_SADDR
+        int4 o;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
+                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + 16u * g));
+        (void)cp;
+#else
         const int4 o = cp[g];
+#endif
         gather(b[4 * g + 0], o.x);
         gather(b[4 * g + 1], o.y);
         gather(b[4 * g + 2], o.z);
@@ -660,7 +688,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       float v[U];
 #pragma unroll
       for (int g = 0; g < U / 4; ++g) {
+#if GESPMM_SADDR
+        float4 x;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + (4u * kStageCap + 16u * g)));
+        (void)vp;
+#else
         const float4 x = vp[g];
+#endif
         v[4 * g] = x.x, v[4 * g + 1] = x.y, v[4 * g + 2] = x.z, v[4 * g + 3] = x.w;
       }
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
