@@ -660,19 +660,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     // 32-bit shared address of stage entry 0 relative to position 0
     const uint32_t s_pos0 = static_cast<uint32_t>(__cvta_generic_to_shared(sc)) - 4u * static_cast<uint32_t>(sbase);
 #endif
+    // the 4 staged offsets / values at positions qb + 4g .. qb + 4g + 3
+    auto stage_off4 = [&](int qb, int g) {
+      int4 o;
+#if GESPMM_SADDR
+      asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
+                   : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + 16u * g));
+#else
+      o = reinterpret_cast<const int4*>(sc + (qb - sbase))[g];
+#endif
+      return o;
+    };
+    auto stage_val4 = [&](int qb, int g) {
+      float4 x;
+#if GESPMM_SADDR
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                   : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + (4u * kStageCap + 16u * g)));
+#else
+      x = reinterpret_cast<const float4*>(sv + (qb - sbase))[g];
+#endif
+      return x;
+    };
     auto issue = [&](int qb, float (&b)[U][CWM][VEC]) {
-      const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
 #pragma unroll
       for (int g = 0; g < U / 4; ++g) {
-#if GESPMM_SADDR
-        int4 o;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
-                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + 16u * g));
-        (void)cp;
-#else
-        const int4 o = cp[g];
-#endif
+        const int4 o = stage_off4(qb, g);
         gather(b[4 * g + 0], o.x);
         gather(b[4 * g + 1], o.y);
         gather(b[4 * g + 2], o.z);
@@ -684,19 +698,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       Vec<VEC>::ld(d[0], r + lane * VEC);
     };
     auto consume = [&](int qb, const float (&b)[U][CWM][VEC]) {
-      const float4* vp = reinterpret_cast<const float4*>(sv + (qb - sbase));
       float v[U];
 #pragma unroll
       for (int g = 0; g < U / 4; ++g) {
-#if GESPMM_SADDR
-        float4 x;
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
-                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + (4u * kStageCap + 16u * g)));
-        (void)vp;
-#else
-        const float4 x = vp[g];
-#endif
+        const float4 x = stage_val4(qb, g);
         v[4 * g] = x.x, v[4 * g + 1] = x.y, v[4 * g + 2] = x.z, v[4 * g + 3] = x.w;
       }
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
@@ -751,19 +756,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
             // (config 3, N=32: 1.539 -> 1.306 ms).
             while (qb >= lo && qb + FB <= min(hi, re)) {
               float bf[FB > 0 ? FB : 4][CWM][VEC];
-              const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
 #pragma unroll
               for (int g = 0; g < FB / 4; ++g) {
-                const int4 o = cp[g];
+                const int4 o = stage_off4(qb, g);
                 gather(bf[4 * g + 0], o.x);
                 gather(bf[4 * g + 1], o.y);
                 gather(bf[4 * g + 2], o.z);
                 gather(bf[4 * g + 3], o.w);
               }
-              const float4* vp = reinterpret_cast<const float4*>(sv + (qb - sbase));
 #pragma unroll
               for (int g = 0; g < FB / 4; ++g) {
-                const float4 x = vp[g];
+                const float4 x = stage_val4(qb, g);
                 fold_pair(x.x, bf[4 * g + 0], x.y, bf[4 * g + 1]);
                 fold_pair(x.z, bf[4 * g + 2], x.w, bf[4 * g + 3]);
               }
