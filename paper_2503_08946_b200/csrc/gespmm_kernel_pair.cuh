@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
   constexpr int H = U / 2;
   constexpr int TW = 16 * VEC;   // columns per column block
   constexpr unsigned FULL = 0xffffffffu;
-  __shared__ __align__(16) int scol[kWarpsPerBlock][kStageCap];
-  __shared__ __align__(16) float sval[kWarpsPerBlock][kStageCap];
+  // per warp: colind slice then vals slice (vals at an immediate offset)
+  __shared__ __align__(16) int stg[kWarpsPerBlock][2 * kStageCap];
   __shared__ int rpw[kWarpsPerBlock][kTileMaxRows + 4];
 
   const int warp = threadIdx.x >> 5;
@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
   const float* bw = P.B + woff;
   const int64_t ldb = P.ldb;
   const int64_t ldc = P.ldc;
-  int* const sc = scol[warp];
-  float* const sv = sval[warp];
+  int* const sc = stg[warp];
+  float* const sv = reinterpret_cast<float*>(stg[warp] + kStageCap);
   int* const rp = rpw[warp];
   const bool accumulate = P.accumulate != 0;
   const bool seed_c0 = accumulate && SR::kSeedC0;
@@ -250,13 +250,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     if (!is_tile && it.y > 0) seed(lo, SR::identity(), nullptr);
     else row_seed(lo, crow);
 
+    // 32-bit shared address of my half's entries of position-block 0
+    const uint32_t s_pos0 = static_cast<uint32_t>(__cvta_generic_to_shared(sc)) +
+                            4u * static_cast<uint32_t>(H * g - sbase);
     for (int qb = sbase; qb < hi; qb += U) {
       // my half's four staged entries of this batch: positions qb + 2i + g
       float b[H][VEC];
       float v[H];
 #pragma unroll
       for (int q4 = 0; q4 < H / 4; ++q4) {
-        const int4 o = *reinterpret_cast<const int4*>(sc + (qb - sbase) + H * g + 4 * q4);
+        int4 o;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
+                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + 16u * q4));
         gather(b[4 * q4 + 0], o.x);
         gather(b[4 * q4 + 1], o.y);
         gather(b[4 * q4 + 2], o.z);
@@ -264,7 +270,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
       }
 #pragma unroll
       for (int q4 = 0; q4 < H / 4; ++q4) {
-        const float4 vv = *reinterpret_cast<const float4*>(sv + (qb - sbase) + H * g + 4 * q4);
+        float4 vv;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(vv.x), "=f"(vv.y), "=f"(vv.z), "=f"(vv.w)
+                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + (4u * kStageCap + 16u * q4)));
         v[4 * q4] = vv.x, v[4 * q4 + 1] = vv.y, v[4 * q4 + 2] = vv.z, v[4 * q4 + 3] = vv.w;
       }
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: the batch is in the current row
