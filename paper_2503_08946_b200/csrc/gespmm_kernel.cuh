@@ -634,28 +634,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     else row_seed(lo, crow);
 
     // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
-    // ring: copy batch qb into slot, one commit group per batch
-    auto issue_ring = [&](int qb, int slot) {
-      float4* dst = ring + slot * (U * RG::kLanesPerRow);
-      // the batch's offsets with 128-bit broadcast loads (no per-row LDS
-      // latency chain); each lane then picks the row it copies
-      int offs[U];
-      const int4* cp = reinterpret_cast<const int4*>(sc + (qb - sbase));
-#pragma unroll
-      for (int g = 0; g < U / 4; ++g) {
-        const int4 o = cp[g];
-        offs[4 * g] = o.x, offs[4 * g + 1] = o.y, offs[4 * g + 2] = o.z, offs[4 * g + 3] = o.w;
-      }
-      const uint64_t pol = policy_evict_last();
-#pragma unroll
-      for (int g = 0; g < U; g += RG::kRowsPerIssue) {
-        int off = offs[g];
-#pragma unroll
-        for (int r = 1; r < RG::kRowsPerIssue; ++r) off = rsub == r ? offs[g + r] : off;
-        cp_async16_b(dst + (g + rsub) * RG::kLanesPerRow + rchunk, rsrc, static_cast<uint32_t>(off), pol);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
 #if GESPMM_SADDR
     // 32-bit shared address of stage entry 0 relative to position 0
     const uint32_t s_pos0 = static_cast<uint32_t>(__cvta_generic_to_shared(sc)) - 4u * static_cast<uint32_t>(sbase);
@@ -682,6 +660,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       x = reinterpret_cast<const float4*>(sv + (qb - sbase))[g];
 #endif
       return x;
+    };
+    // ring: copy batch qb into slot, one commit group per batch
+    auto issue_ring = [&](int qb, int slot) {
+      float4* dst = ring + slot * (U * RG::kLanesPerRow);
+      // the batch's offsets with 128-bit broadcast loads (no per-row LDS
+      // latency chain); each lane then picks the row it copies
+      int offs[U];
+#pragma unroll
+      for (int g = 0; g < U / 4; ++g) {
+        const int4 o = stage_off4(qb, g);
+        offs[4 * g] = o.x, offs[4 * g + 1] = o.y, offs[4 * g + 2] = o.z, offs[4 * g + 3] = o.w;
+      }
+      const uint64_t pol = policy_evict_last();
+#pragma unroll
+      for (int g = 0; g < U; g += RG::kRowsPerIssue) {
+        int off = offs[g];
+#pragma unroll
+        for (int r = 1; r < RG::kRowsPerIssue; ++r) off = rsub == r ? offs[g + r] : off;
+        cp_async16_b(dst + (g + rsub) * RG::kLanesPerRow + rchunk, rsrc, static_cast<uint32_t>(off), pol);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto issue = [&](int qb, float (&b)[U][CWM][VEC]) {
 #pragma unroll
