@@ -101,6 +101,44 @@ void oracle_spmm_absbound_f64(int64_t M, int64_t N, const int32_t* rowptr, const
     }
 }
 
+/* (1b) The reference restatement for every reduce op, on fp32 inputs, in
+ * fp64 (the interpreter's number type, oracle.cpp:337-352): products
+ * val*B are exact in fp64 (24 + 24 significand bits); SUM is the reference's
+ * ascending, unfused c = c + prod from c = 0 (gespmm_alg2.mir:51-59,
+ * oracle.cpp:593-613); MEAN = SUM / deg; MAX/MIN = the largest/smallest exact
+ * product (the semiring extension).  Empty rows give 0.
+ * bound[i,j] = sum_p |val*B| (MEAN: / deg), the scale of the north star's
+ * norm-wise 1e-5 tolerance.  Because fp32 rounding is monotone, a correct fp32
+ * MAX/MIN equals (float) of this value exactly. */
+void oracle_spmm_ref64_op(int64_t M, int64_t N, const int32_t* rowptr, const int32_t* colind,
+                          const float* vals, const float* B, int64_t ldb, double* out,
+                          double* bound, int op, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t i = 0; i < M; ++i) {
+    const int64_t rs = rowptr[i], re = rowptr[i + 1], deg = re - rs;
+    for (int64_t j = 0; j < N; ++j) {
+      double c = 0.0, s = 0.0;
+      for (int64_t p = rs; p < re; ++p) {
+        const double prod = (double)vals[p] * (double)B[(int64_t)colind[p] * ldb + j];
+        s += fabs(prod);
+        if (op == OR_SUM || op == OR_MEAN) c = c + prod;
+        else if (p == rs) c = prod;
+        else if (op == OR_MAX) c = prod > c ? prod : c;
+        else c = prod < c ? prod : c;
+      }
+      if (op == OR_MEAN && deg) {
+        c /= (double)deg;
+        s /= (double)deg;
+      }
+      out[i * N + j] = c;
+      bound[i * N + j] = s;
+    }
+  }
+}
+
 /* ---- (2) the fp32 twin ---------------------------------------------------- */
 
 /* pick(op, a, b): the max/min fold step, IEEE 754-2019 maximumNumber /

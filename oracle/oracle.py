@@ -56,6 +56,9 @@ def lib():
         L.oracle_spmm_absbound_f64.argtypes = [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr,
                                                _i64, ctypes.c_int]
         L.oracle_spmm_absbound_f64.restype = None
+        L.oracle_spmm_ref64_op.argtypes = [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr,
+                                           ctypes.c_int, ctypes.c_int]
+        L.oracle_spmm_ref64_op.restype = None
         L.oracle_spmm_f32.argtypes = [_i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _i64,
                                       ctypes.c_int, ctypes.c_int, _i64, ctypes.c_int]
         L.oracle_spmm_f32.restype = ctypes.c_int
@@ -112,6 +115,37 @@ def spmm_ref_f64(rowptr, colind, vals, B, C0=None, nthreads: int = 0) -> np.ndar
     lib().oracle_spmm_ref_f64(M, N, _p(rowptr), _p(colind), _p(vals), _p(B), N, _p(C), N,
                               nthreads)
     return C
+
+
+def spmm_ref64_op(rowptr, colind, vals, B, op="sum", nthreads: int = 0):
+    """The reference restatement for every reduce op in fp64 on fp32 inputs
+    (oracle_spmm_ref64_op): returns (value f64 [M, N], bound f64 [M, N]) with
+    bound = sum_p |val*B| (mean: / deg), the north star's tolerance scale."""
+    rowptr = _c(rowptr, np.int32)
+    colind = _c(colind, np.int32)
+    vals = _c(vals, np.float32)
+    B = _c(B, np.float32)
+    M, N = len(rowptr) - 1, B.shape[1]
+    out = np.zeros((M, N), np.float64)
+    bound = np.zeros((M, N), np.float64)
+    lib().oracle_spmm_ref64_op(M, N, _p(rowptr), _p(colind), _p(vals), _p(B), N, _p(out),
+                               _p(bound), OPS[op] if isinstance(op, str) else int(op), nthreads)
+    return out, bound
+
+
+def ref64_error_ratio(got, ref, bound, op="sum"):
+    """North-star parity of a GPU result against the fp64 reference
+    restatement: sum/mean -> max |got - ref| / (1e-5 * max(|ref|, bound))
+    (<= 1 passes); max/min -> the number of cells where got != (float32)ref
+    (0 passes: bit-exact up to the sign of zero)."""
+    got = np.asarray(got)
+    if op in ("max", "min"):
+        return int(np.count_nonzero(got.astype(np.float32) != ref.astype(np.float32)))
+    scale = np.maximum(np.abs(ref), bound)
+    err = np.abs(got.astype(np.float64) - ref)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        r = np.where(scale > 0, err / (1e-5 * scale), np.where(err > 0, np.inf, 0.0))
+    return float(r.max()) if r.size else 0.0
 
 
 def spmm_absbound(rowptr, colind, vals, B, nthreads: int = 0) -> np.ndarray:

@@ -81,6 +81,20 @@ namespace {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// A plan lives on the device it was built on: its calls switch to that device
+// for their duration (workspace allocations, counters and launches) and
+// restore the caller's current device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Shape/argument checks shared by the device and host entry points.
 gespmm_status_t check_shape(int64_t M, int64_t K, int64_t N, int64_t nnz, int64_t ldb,
                             int64_t ldc) {
@@ -359,6 +373,10 @@ gespmm_status_t gespmm_validate_csr_device(int64_t M, int64_t K, int64_t nnz,
                                            void* stream) {
   g_last_error.clear();
   if (M < 0 || K < 0 || nnz < 0) return fail(GESPMM_INVALID_ARG, "invalid argument: negative size");
+  gespmm_status_t st0 = check_shape(M, K, 1, nnz, 1, 1);
+  if (st0 != GESPMM_OK) return st0;
+  if ((M > 0 && !rowptr) || (nnz > 0 && !colind))
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
   gespmm_plan_s tmp;
   tmp.M = M;
   tmp.K = K;
@@ -401,6 +419,9 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, int64_t N, const int32_t
   if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
     return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
   if (plan->n_items == 0) return GESPMM_OK;  // M == 0
+  if (!rowptr || (plan->nnz > 0 && (!colind || !vals || !B)) || !C)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
+  DeviceGuard dg(plan->device);
   return execute_range(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, nullptr,
                        nullptr, as_stream(stream));
 }
@@ -418,6 +439,9 @@ gespmm_status_t gespmm_plan_execute_rows(gespmm_plan_t plan, int64_t row_begin, 
   if (row_begin < 0 || row_end < row_begin || row_end > plan->M)
     return fail(GESPMM_INVALID_ARG, "invalid argument: need 0 <= row_begin <= row_end <= M");
   if (plan->n_items == 0 || row_end == row_begin) return GESPMM_OK;
+  if (!rowptr || (plan->nnz > 0 && (!colind || !vals || !B)) || !C)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
+  DeviceGuard dg(plan->device);
   cudaStream_t s = as_stream(stream);
   if (!plan->row_range) {
     cudaError_t e = cudaMalloc(&plan->row_range, 4 * sizeof(int64_t));
@@ -446,6 +470,9 @@ gespmm_status_t gespmm_plan_execute_peers(gespmm_plan_t plan, int64_t N, const i
   for (int q = 0; q < n_peers; ++q)
     if (!peers[q]) return fail(GESPMM_INVALID_ARG, "invalid argument: null peer buffer");
   if (plan->n_items == 0) return GESPMM_OK;
+  if (!rowptr || (plan->nnz > 0 && (!colind || !vals || !B)) || !C)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
+  DeviceGuard dg(plan->device);
   return execute_range(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, nullptr, nullptr,
                        as_stream(stream), peers, n_peers, peer_row0 * ldc);
 }
@@ -491,6 +518,7 @@ gespmm_status_t gespmm_ipc_close_handle(void* dev_ptr) {
 
 gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
   if (!plan) return GESPMM_OK;
+  DeviceGuard dg(plan->device);
   if (plan->work_ctr) cudaFree(plan->work_ctr);
   if (plan->row_range) cudaFree(plan->row_range);
   if (plan->items) cudaFree(plan->items);
@@ -521,7 +549,10 @@ gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
   g_last_error.clear();
   gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
   if (st != GESPMM_OK) return st;
-  if (M > 0 && !rowptr) return fail(GESPMM_INVALID_ARG, "invalid argument: rowptr is null");
+  if ((M > 0 && !rowptr) || (nnz > 0 && (!colind || !vals)) || (K * N > 0 && !B) || (M * N > 0 && !C))
+    return fail(GESPMM_INVALID_ARG, "invalid argument: null pointer");
+  if (op < GESPMM_REDUCE_SUM || op > GESPMM_REDUCE_MEAN)
+    return fail(GESPMM_INVALID_ARG, "invalid argument: unknown reduce op");
   // A per-device plan object re-planned in place (no cudaMalloc/cudaFree per
   // call: cudaFree synchronizes the device); the call returns after its
   // launches drain, so the next call may reuse the plan's buffers.
@@ -736,7 +767,9 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   if (st != GESPMM_OK) return st;
   if (e != cudaSuccess) return cuda_fail(e, "pipelined host spmm");
   // C's contents are unspecified after CSR_INVALID (earlier chunks may have
-  // been written back); no launch ever read an out-of-range colind.
+  // been written back); no launch ever read an out-of-range colind: every
+  // launch follows its chunk's colind check on `s` and returns at once when
+  // the flag is set (single chunk included).
   if (h_err) return fail(GESPMM_CSR_INVALID, csr_error_message(h_err, K));
   return GESPMM_OK;
 }

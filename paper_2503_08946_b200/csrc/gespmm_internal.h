@@ -98,8 +98,9 @@ struct KParams {
   int idx_aligned;         // colind and vals 16-byte aligned -> 128-bit staging loads
   int off32;               // K*ldb <= 2^32: stage 32-bit B-row element offsets
   // Pipelined host path (gespmm_csr_spmm_host): the launch runs items
-  // [range[0], range[1]) only (nullptr: all), and returns at once when
-  // *abort_flag is set (a failed on-device colind check of an earlier chunk).
+  // [range[0], range[1]) only (nullptr: all); it returns at once when
+  // abort_flag is non-null and *abort_flag is set (a failed on-device colind
+  // check of this or an earlier chunk, with or without a range).
   const int64_t* range;
   const int* abort_flag;
   // Fused C all-gather (gespmm_plan_execute_peers): every C row is also stored

@@ -130,8 +130,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
 
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
   int64_t t_begin = 0, t_end = P.n_items;
+  // a failed on-device colind check earlier on the stream (host entry point,
+  // single- or multi-chunk): no item is gathered through an invalid colind
+  if (P.abort_flag && *reinterpret_cast<const volatile int*>(P.abort_flag)) return;
   if (P.range) {  // one chunk of the pipelined host path
-    if (*reinterpret_cast<const volatile int*>(P.abort_flag)) return;
     t_begin = P.range[0];
     t_end = P.range[1];
   }

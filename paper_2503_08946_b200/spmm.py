@@ -79,10 +79,12 @@ class Plan:
         self.colind = colind
         self.device = rowptr.device
         h = ctypes.c_void_p()
-        _lib.check(_L.gespmm_plan_create(ctypes.byref(h), self.M, self.K, self.nnz,
-                                         rowptr.data_ptr(), colind.data_ptr(),
-                                         1 if validate else 0,
-                                         _stream_handle(stream, self.device)))
+        # the plan is built on (and remembers) the device its rowptr lives on
+        with _torch().cuda.device(self.device):
+            _lib.check(_L.gespmm_plan_create(ctypes.byref(h), self.M, self.K, self.nnz,
+                                             rowptr.data_ptr(), colind.data_ptr(),
+                                             1 if validate else 0,
+                                             _stream_handle(stream, self.device)))
         self._h = h
 
     def info(self) -> dict:
@@ -170,10 +172,11 @@ def csr_spmm(rowptr, colind, vals, B, reduce="sum", out=None, accumulate: bool =
             raise Error(ErrorKind.InvalidArgument, "accumulate=True needs out (C0)")
         out = torch.empty((M, N), dtype=torch.float32, device=B.device)
     _check_dense("out", out)
-    _lib.check(_L.gespmm_csr_spmm(M, K, N, colind.numel(), rowptr.data_ptr(), colind.data_ptr(),
-                                  vals.data_ptr(), B.data_ptr(), B.stride(0), out.data_ptr(),
-                                  out.stride(0), _reduce_code(reduce), 1 if accumulate else 0,
-                                  _stream_handle(stream, B.device)))
+    with torch.cuda.device(B.device):
+        _lib.check(_L.gespmm_csr_spmm(M, K, N, colind.numel(), rowptr.data_ptr(), colind.data_ptr(),
+                                      vals.data_ptr(), B.data_ptr(), B.stride(0), out.data_ptr(),
+                                      out.stride(0), _reduce_code(reduce), 1 if accumulate else 0,
+                                      _stream_handle(stream, B.device)))
     return out
 
 
@@ -200,10 +203,10 @@ def csr_spmm_host(rowptr, colind, vals, B, reduce="sum", C0=None, out=None):
     K, N = B.shape
     accumulate = C0 is not None
     if out is None:
-        if isinstance(B, torch.Tensor):
-            out = torch.empty((M, N), dtype=torch.float32, pin_memory=B.is_pinned())
-        else:
-            out = np.zeros((M, N), np.float32)
+        # pinned by default: a device-to-host copy into pageable memory blocks
+        # the issuing thread, which would serialize the pipelined chunks
+        pinned = torch.empty((M, N), dtype=torch.float32, pin_memory=torch.cuda.is_available())
+        out = pinned if isinstance(B, torch.Tensor) else pinned.numpy()
     if accumulate:
         if isinstance(out, torch.Tensor):
             out.copy_(torch.as_tensor(C0))

@@ -38,3 +38,14 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+def record_parity(test: str, **fields) -> None:
+    """Appends one JSON line of parity evidence (max error ratios against the
+    fp64 reference restatement) to $GESPMM_PARITY_OUT when it is set; the GPU
+    runs point it into gpurun_out/ and the summary is committed under profiles/."""
+    path = os.environ.get("GESPMM_PARITY_OUT")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"test": test, **fields}) + "\n")

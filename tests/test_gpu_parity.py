@@ -442,6 +442,32 @@ def test_host_entry_point_pipelined_invalid_colind(cuda, oracle_mod):
     np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG))
 
 
+@pytest.mark.parametrize("badval", [-1, -(2**31), 7_000_000])
+def test_host_entry_point_single_chunk_invalid_colind(cuda, oracle_mod, badval):
+    """Small M (one chunk, no item range): a negative or huge column is caught
+    by the on-device check and the launch returns without gathering through it
+    (with 32-bit offsets a negative column would wrap ~16 GB past B) -- a clean
+    CsrInvalid, no sticky CUDA error, and the next call works."""
+    import torch
+
+    from paper_2503_08946_b200.errors import Error, ErrorKind
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    rng = np.random.default_rng(43)
+    M, K, N = 300, 200, 128
+    rowptr, colind, vals = random_csr(rng, M, K, 0.05, long_rows=[(7, 700)])
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    for pos in (0, int(rowptr[-1]) // 2, int(rowptr[-1]) - 1):
+        bad = colind.copy()
+        bad[pos] = badval
+        with pytest.raises(Error) as ei:
+            csr_spmm_host(rowptr, bad, vals, B, "sum")
+        assert ei.value.kind == ErrorKind.CsrInvalid
+        torch.cuda.synchronize()  # no sticky error from an out-of-bounds gather
+    got = csr_spmm_host(rowptr, colind, vals, B, "sum")
+    np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, "sum", seg_len=SEG))
+
+
 @pytest.mark.parametrize("op", ["sum", "min"])
 def test_host_entry_point_front_loaded_chunks(cuda, oracle_mod, op):
     """Nonzeros piled into the first rows (as in R-MAT): the host pipeline runs
@@ -553,12 +579,22 @@ def test_config2_full_size_bit_exact(cuda, oracle_mod, op):
     np.testing.assert_array_equal(got.cpu().numpy(), want)
 
 
-def sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3000, seed=0):
-    """Checks C on a sample of rows (the longest rows, random rows, the first
-    and last rows) against the twin, bit for bit, without moving the full B to
-    the host: each sampled row's result depends only on its own nonzeros and
-    the B rows they name, so the sub-problem uses a compacted B."""
+def sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3000, seed=0, tag=""):
+    """Checks C on a sample of rows (the 16 longest rows, random rows, the first
+    and last rows) without moving the full B to the host: each sampled row's
+    result depends only on its own nonzeros and the B rows they name, so the
+    sub-problem uses a compacted B.  Two checks per row:
+      * bit for bit against the fp32 twin (oracle_spmm_f32);
+      * against the fp64 reference restatement (oracle_spmm_ref64_op: the
+        reference interpreter's ascending, unfused fp64 sum,
+        gespmm_alg2.mir:38-59, oracle.cpp:593-613): sum/mean within the north
+        star's 1e-5 norm-wise bound |gpu - ref| <= 1e-5 max(|ref|, sum|v b|),
+        max/min equal to (float) ref exactly.
+    Returns (rows, nnz, ratio) -- ratio = max |gpu-ref| / (1e-5 scale) for
+    sum/mean, mismatching cells for max/min."""
     import torch
+
+    from conftest import record_parity
 
     rp = csr.rowptr.long()
     deg = (rp[1:] - rp[:-1])
@@ -574,17 +610,32 @@ def sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3000, seed=0):
         torch.arange(int(srp[-1]), device=rp.device) - torch.repeat_interleave(srp[:-1], sdeg))
     cols = csr.colind.long()[pos]
     ucols, inv = torch.unique(cols, return_inverse=True)
-    want = oracle_mod.spmm_f32(srp.int().cpu().numpy(), inv.int().cpu().numpy(),
-                               csr.vals[pos].cpu().numpy(), B[ucols].cpu().numpy(), op, seg_len=SEG)
-    np.testing.assert_array_equal(C[rows].cpu().numpy(), want)
-    return int(rows.numel()), int(srp[-1])
+    srp_h, inv_h, v_h, B_h = (srp.int().cpu().numpy(), inv.int().cpu().numpy(), csr.vals[pos].cpu().numpy(),
+                              B[ucols].cpu().numpy())
+    got = C[rows].cpu().numpy()
+    want = oracle_mod.spmm_f32(srp_h, inv_h, v_h, B_h, op, seg_len=SEG)
+    np.testing.assert_array_equal(got, want)
+    ref, bound = oracle_mod.spmm_ref64_op(srp_h, inv_h, v_h, B_h, op)
+    ratio = oracle_mod.ref64_error_ratio(got, ref, bound, op)
+    record_parity("sampled_rows_vs_ref64", workload=tag, op=op, N=int(B.shape[1]), rows=int(rows.numel()),
+                  nnz=int(srp[-1]), max_row_nnz=int(sdeg.max()), ratio=ratio,
+                  metric="max|gpu-ref64|/(1e-5*max(|ref|,sum|vb|))" if op in ("sum", "mean")
+                  else "cells != (float)ref64")
+    if op in ("sum", "mean"):
+        assert ratio <= 1.0, f"{tag} {op}: error {ratio:.3g} x the 1e-5 norm-wise bound"
+    else:
+        assert ratio == 0, f"{tag} {op}: {ratio} cells differ from (float) of the fp64 reference"
+    return int(rows.numel()), int(srp[-1]), ratio
 
 
-@pytest.mark.parametrize("workload", ["config4", "config5", "config3"])
-def test_full_size_configs_sampled_bit_exact(cuda, oracle_mod, workload):
-    """BASELINE configs 3-5 at full size (R-MAT scale 22/64M and scale 24/2^30
-    edges with N=128, Reddit-like 114.6M nnz with N=256 in column panels) on one
-    GPU: every op bit-exact to the twin on sampled rows incl. the longest rows."""
+@pytest.mark.parametrize("workload,N", [("config2", 64), ("config4", 64), ("config4", 128), ("config4", 256),
+                                        ("config5", 128), ("config3", 256)])
+def test_full_size_configs_sampled_bit_exact(cuda, oracle_mod, workload, N):
+    """BASELINE configs 2-5 at full size (R-MAT scale 20/16M with N=64, scale
+    22/64M with N=64/128/256, scale 24/2^30 edges with N=128, Reddit-like
+    114.6M nnz with N=256 in column panels) on one GPU: every op bit-exact to
+    the twin AND within the north-star bound of the fp64 reference (max/min
+    exact) on sampled rows incl. the 16 longest rows (up to ~10^5 nonzeros)."""
     import torch
 
     from paper_2503_08946_b200 import workloads as W
@@ -592,18 +643,18 @@ def test_full_size_configs_sampled_bit_exact(cuda, oracle_mod, workload):
 
     if workload == "config3":
         csr = W.reddit_like_csr(device=cuda)
-        N = 256
     else:
-        scale, edges = (22, 64 * 2**20) if workload == "config4" else (24, 2**30)
+        scale, edges = {"config2": (20, 16 * 2**20), "config4": (22, 64 * 2**20),
+                        "config5": (24, 2**30)}[workload]
         csr = W.rmat_csr_gpu(scale, edges, seed=3, device=cuda)
-        N = 128
     B = W.dense_gpu(csr.K, N, seed=2, device=cuda)
     plan = Plan(csr.rowptr, csr.colind, csr.K)
     C = torch.empty((csr.M, N), dtype=torch.float32, device=cuda)
     for op in OPS:
         plan.execute(csr.vals, B, op, out=C)
         torch.cuda.synchronize()
-        sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=2000 if workload == "config5" else 3000)
+        sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=2000 if workload == "config5" else 3000,
+                               tag=f"{workload}-N{N}")
 
 
 def test_reference_side_cpp_adapter(cuda, tmp_path):
@@ -627,8 +678,18 @@ def test_reference_side_cpp_adapter(cuda, tmp_path):
         assert out.returncode == 0, out.stderr
         got = np.array([float(x) for x in out.stdout.split()], np.float64)
         ref = np.asarray(g["C"], np.float64)
-        scale = np.maximum(np.abs(ref), 1.0)
-        assert np.all(np.abs(got - ref) <= 1e-5 * scale * 64), np.abs(got - ref).max()
+        # the north star's norm-wise bound: 1e-5 max(|ref|, |C0| + sum_p |v b|)
+        M, N, K = g["M"], g["N"], g["K"]
+        rp = np.asarray(g["rowptr"], np.int64)
+        ci = np.asarray(g["colind"], np.int64)
+        v = np.abs(np.asarray(g["vals"], np.float64))
+        Bm = np.abs(np.asarray(g["B"], np.float64).reshape(K, N))
+        bound = np.abs(np.asarray(g["C0"], np.float64).reshape(M, N)).copy()
+        for i in range(M):
+            for p in range(rp[i], rp[i + 1]):
+                bound[i] += v[p] * Bm[ci[p]]
+        tol = 1e-5 * np.maximum(np.abs(ref), bound.reshape(-1))
+        assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
 @pytest.mark.parametrize("mode", [-1, 1])

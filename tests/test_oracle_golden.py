@@ -95,3 +95,27 @@ def test_live_reference_rerun(oracle_mod, name):
                                              nthreads=2, C0=C0[:rows, :cols])
     got[:rows, :cols] = Cr
     np.testing.assert_array_equal(got, C)
+
+
+def test_ref64_op_sum_is_the_pinned_reference(oracle_mod):
+    """oracle_spmm_ref64_op (the per-op fp64 restatement the GPU parity tests
+    hold every op to) computes, for sum, exactly the reference interpreter's
+    C on config 1 (the golden sha256 of tests/golden/config1_checksum.json)."""
+    from paper_2503_08946_b200 import workloads as W
+
+    g = load_golden("config1_checksum.json")
+    csr = W.uniform_csr(4096, 4096, 0.01, seed=1)
+    B = W.dense(4096, 32, seed=2)
+    C, bound = oracle_mod.spmm_ref64_op(csr.rowptr, csr.colind, csr.vals, B, "sum")
+    assert hashlib.sha256(C.tobytes()).hexdigest() == g["c_f64_sha256"]
+    assert np.all(bound >= np.abs(C))
+    # max/min: (float) of the exact fp64 extreme product is what a correct fp32
+    # max/min must produce; the fp32 twin agrees everywhere
+    for op in ("max", "min"):
+        ref, _ = oracle_mod.spmm_ref64_op(csr.rowptr, csr.colind, csr.vals, B, op)
+        twin = oracle_mod.spmm_f32(csr.rowptr, csr.colind, csr.vals, B, op, seg_len=256)
+        assert oracle_mod.ref64_error_ratio(twin, ref, None, op) == 0
+    for op in ("sum", "mean"):
+        ref, bound = oracle_mod.spmm_ref64_op(csr.rowptr, csr.colind, csr.vals, B, op)
+        twin = oracle_mod.spmm_f32(csr.rowptr, csr.colind, csr.vals, B, op, seg_len=256)
+        assert oracle_mod.ref64_error_ratio(twin, ref, bound, op) <= 1.0

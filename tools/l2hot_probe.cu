@@ -1,0 +1,493 @@
+// l2hot_probe.cu -- how much of the large-R-MAT DRAM traffic an L2 hot set
+// can remove (VERDICT r1 "Next" 3).
+//
+// Replays a column stream (a CSR's colind) as 512-byte B-row gathers (N=128
+// fp32, one 16-byte LDG per lane), the SpMM's order: each warp walks
+// contiguous spans of `span` positions, U rows in flight.  Nothing else is
+// read or written, so the time and DRAM bytes isolate the B gathers.
+//
+// idx entries carry a hot flag in bit 31 (set by the caller from the column
+// degrees).  Modes:
+//   0  plain loads (no cache hint)
+//   1  hot rows L2::evict_last, cold rows L2::evict_first (per-lane policy select)
+//   2  hot rows evict_last, cold rows evict_normal
+//   3  hot rows normal, cold rows evict_first
+//   4  hot rows from a compact copy (hot index in the low bits), cold rows
+//      plain -- with an access-policy window on the copy set by the caller
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+template <int VEC>
+struct VT;
+template <>
+struct VT<1> { using T = float; };
+template <>
+struct VT<2> { using T = float2; };
+template <>
+struct VT<4> { using T = float4; };
+
+__device__ __forceinline__ void ldh(float& d, const float* p, uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(d) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ldh(float2& d, const float* p, uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(d.x), "=f"(d.y) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ldh(float4& d, const float* p, uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(d.x), "=f"(d.y), "=f"(d.z), "=f"(d.w) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ float sum(float v) { return v; }
+__device__ __forceinline__ float sum(float2 v) { return v.x + v.y; }
+__device__ __forceinline__ float sum(float4 v) { return v.x + v.y + v.z + v.w; }
+
+// Row-width generic form: each row gathers 32*VEC floats at column offset
+// `col0` of a 128-wide B (one column panel of a panelled execution).
+template <int U, int MODE, int VEC>
+__global__ void __launch_bounds__(256, U * VEC <= 32 ? 4 : U * VEC <= 64 ? 2 : 1)
+    probe_w(const float* __restrict__ B, const int* __restrict__ idx, int64_t nidx, int span, int col0,
+            float* sink) {
+  using T = typename VT<VEC>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t pl, pf, pn;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pn));
+  float a0 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    for (int64_t base = s0; base < s1; base += U) {
+      const int my = (lane < U && base + lane < s1) ? __ldg(idx + base + lane) : 0;
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = __shfl_sync(0xffffffffu, my, u);
+        const bool hot = e < 0;
+        const uint32_t r = static_cast<uint32_t>(e) & 0x7fffffffu;
+        const float* src = B + static_cast<int64_t>(r) * 128 + col0 + VEC * lane;
+        const uint64_t pol = MODE == 0 ? pn : MODE == 1 ? (hot ? pl : pf) : MODE == 2 ? (hot ? pl : pn) : (hot ? pn : pf);
+        ldh(v[u], src, pol);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) a0 += sum(v[u]);
+    }
+  }
+  if (a0 == 1234.5f) sink[0] = a0;
+}
+
+// Panelled replay: 128 / (32*vec) passes over idx, one per column panel
+// (same stream order per pass); returns the best total of `reps` (ms).
+// Bulk-copy ring: each warp owns D slots of U rows in shared memory; batch k
+// is fetched by U lanes issuing one cp.async.bulk (global -> shared, the row's
+// 32*VEC floats) each, completion tracked by the slot's mbarrier (expect_tx
+// armed by lane 0 first); rows are read back with one LDS per lane per row.
+// No registers hold in-flight rows, one instruction moves a whole row.
+template <int U, int D, int VEC, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    probe_bulk(const float* __restrict__ B, const int* __restrict__ idx, int64_t nidx, int span, int col0,
+               float* sink) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int RB = 128 * VEC;  // row bytes
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* ring = smraw + wib * (D * U * RB);
+  __shared__ __align__(8) unsigned long long bar[8][D];
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t pl, pf;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  if (lane < D) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][lane]));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t phase = 0;  // bit d: parity of slot d
+  float a0 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    const int nb = static_cast<int>((s1 - s0 + U - 1) / U);
+    auto issue = [&](int k) {
+      if (k >= nb) return;
+      const int d = k % D;
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
+      const int64_t p = s0 + static_cast<int64_t>(k) * U + lane;
+      const int nrow = static_cast<int>(s1 - (s0 + static_cast<int64_t>(k) * U) < U ? s1 - (s0 + static_cast<int64_t>(k) * U) : U);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nrow * RB) : "memory");
+      __syncwarp();
+      if (lane < nrow) {
+        const int e = __ldg(idx + p);
+        const bool hot = e < 0;
+        const uint32_t r = static_cast<uint32_t>(e) & 0x7fffffffu;
+        const float* src = B + static_cast<int64_t>(r) * 128 + col0;
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(ring + (d * U + lane) * RB));
+        if (MODE == 1) {
+          const uint64_t pol = hot ? pl : pf;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+              "l"(src), "n"(RB), "r"(b), "l"(pol)
+              : "memory");
+        } else {
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                       "l"(src), "n"(RB), "r"(b)
+                       : "memory");
+        }
+      }
+    };
+    for (int k = 0; k < D - 1; ++k) issue(k);
+    for (int k = 0; k < nb; ++k) {
+      issue(k + D - 1);
+      const int d = k % D;
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
+      const uint32_t par = (phase >> d) & 1u;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(b), "r"(par) : "memory");
+      phase ^= 1u << d;
+      const int nrow = static_cast<int>(s1 - (s0 + static_cast<int64_t>(k) * U) < U ? s1 - (s0 + static_cast<int64_t>(k) * U) : U);
+#pragma unroll 4
+      for (int u = 0; u < nrow; ++u) {
+        const float* row = reinterpret_cast<const float*>(ring + (d * U + u) * RB);
+        if (VEC == 4) {
+          const float4 v = reinterpret_cast<const float4*>(row)[lane];
+          a0 += v.x + v.y + v.z + v.w;
+        } else if (VEC == 2) {
+          const float2 v = reinterpret_cast<const float2*>(row)[lane];
+          a0 += v.x + v.y;
+        } else {
+          a0 += row[lane];
+        }
+      }
+      __syncwarp();  // slot d is refilled by issue(k + D)
+    }
+  }
+  if (a0 == 1234.5f) sink[0] = a0;
+}
+
+extern "C" float l2hot_probe_bulk(const float* B, const int* idx, int64_t nidx, int mode, int vec, int U, int D,
+                                  int span, int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = 8 * D * U * 128 * vec;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  const int grid = sms * blocks_per_sm;
+  const int w = 32 * vec;
+#define KB(UU, DD, VV, MM) probe_bulk<UU, DD, VV, MM>
+#define SETA(UU, DD, VV, MM) cudaFuncSetAttribute(KB(UU, DD, VV, MM), cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+#define RUN(UU, DD, VV, MM) KB(UU, DD, VV, MM)<<<grid, 256, smem>>>(B, idx, nidx, span, c0, sink)
+#define ALL(X, MM)                                                          \
+  if (vec == 2 && U == 16 && D == 2) X(16, 2, 2, MM);                      \
+  else if (vec == 2 && U == 16 && D == 4) X(16, 4, 2, MM);                 \
+  else if (vec == 2 && U == 32 && D == 2) X(32, 2, 2, MM);                 \
+  else if (vec == 4 && U == 8 && D == 4) X(8, 4, 4, MM);                   \
+  else if (vec == 4 && U == 16 && D == 2) X(16, 2, 4, MM);                 \
+  else if (vec == 4 && U == 8 && D == 2) X(8, 2, 4, MM);                   \
+  else if (vec == 1 && U == 32 && D == 2) X(32, 2, 1, MM);                 \
+  else X(8, 2, 2, MM);
+  if (mode == 1) { ALL(SETA, 1) } else { ALL(SETA, 0) }
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaDeviceSynchronize();
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    for (int c0 = 0; c0 < 128; c0 += w) {
+      if (mode == 1) { ALL(RUN, 1) } else { ALL(RUN, 0) }
+    }
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 1 && ms < best) best = ms;
+  }
+#undef ALL
+#undef RUN
+#undef SETA
+#undef KB
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? best : -static_cast<float>(err);
+}
+
+extern "C" float l2hot_probe_panels(const float* B, const int* idx, int64_t nidx, int mode, int vec, int span,
+                                    int blocks_per_sm, int reps, float* sink, void* flush, int64_t flush_bytes,
+                                    int U) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  const int grid = sms * blocks_per_sm;
+  const int w = 32 * vec;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaDeviceSynchronize();
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    for (int c0 = 0; c0 < 128; c0 += w) {
+#define L(M, V)                                                                       \
+  (U == 16 ? probe_w<16, M, V><<<grid, 256>>>(B, idx, nidx, span, c0, sink)          \
+           : U == 32 ? probe_w<32, M, V><<<grid, 256>>>(B, idx, nidx, span, c0, sink) \
+                     : probe_w<8, M, V><<<grid, 256>>>(B, idx, nidx, span, c0, sink))
+#define LV(M) (vec == 1 ? L(M, 1) : vec == 2 ? L(M, 2) : L(M, 4))
+      switch (mode) {
+        case 1: LV(1); break;
+        case 2: LV(2); break;
+        case 3: LV(3); break;
+        default: LV(0); break;
+      }
+#undef LV
+#undef L
+    }
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 1 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? best : -static_cast<float>(err);
+}
+
+template <int U, int MODE>
+__global__ void __launch_bounds__(256, 4)
+    probe_hot(const float* __restrict__ B, const float* __restrict__ H, const int* __restrict__ idx,
+              int64_t nidx, int span, float* sink) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t pl, pf;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  uint64_t pn;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pn));
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    for (int64_t base = s0; base < s1; base += U) {
+      const int my = (lane < U && base + lane < s1) ? __ldg(idx + base + lane) : 0;
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = __shfl_sync(0xffffffffu, my, u);
+        const bool hot = e < 0;
+        const uint32_t r = static_cast<uint32_t>(e) & 0x7fffffffu;
+        if (MODE == 0) {
+          v[u] = __ldg(reinterpret_cast<const float4*>(B + static_cast<int64_t>(r) * 128) + lane);
+        } else if (MODE == 4) {
+          const float* src = (hot ? H : B) + static_cast<int64_t>(r) * 128;
+          v[u] = __ldg(reinterpret_cast<const float4*>(src) + lane);
+        } else {
+          const uint64_t pol = MODE == 1 ? (hot ? pl : pf) : MODE == 2 ? (hot ? pl : pn) : (hot ? pn : pf);
+          const float* src = B + static_cast<int64_t>(r) * 128 + 4 * lane;
+          asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                       : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                       : "l"(src), "l"(pol));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a0 += v[u].x + v[u].z;
+        a1 += v[u].y + v[u].w;
+      }
+    }
+  }
+  if (a0 == 1234.5f) sink[0] = a1;
+}
+
+// Returns the best of `reps` timed runs (ms), L2 flushed before each; -1 on error.
+// persist_bytes >= 0: cudaLimitPersistingL2CacheSize is set to it first;
+// win_bytes > 0 (mode 4): an access-policy window [H, H + win_bytes) persisting.
+extern "C" float l2hot_probe(const float* B, const float* H, const int* idx, int64_t nidx, int mode,
+                             int span, int blocks_per_sm, int reps, float* sink, void* flush,
+                             int64_t flush_bytes, int64_t persist_bytes, int64_t win_bytes, float hit_ratio) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (persist_bytes >= 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(persist_bytes));
+  cudaStream_t s = 0;
+  cudaStreamCreate(&s);
+  if (win_bytes > 0) {
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.base_ptr = const_cast<float*>(H);
+    a.accessPolicyWindow.num_bytes = static_cast<size_t>(win_bytes);
+    a.accessPolicyWindow.hitRatio = hit_ratio;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a);
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  const int grid = sms * blocks_per_sm;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaStreamSynchronize(s);
+    cudaCtxResetPersistingL2Cache();  // no hot lines carried over from the previous rep
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes, s);
+    cudaEventRecord(e0, s);
+    switch (mode) {
+      case 1: probe_hot<8, 1><<<grid, 256, 0, s>>>(B, H, idx, nidx, span, sink); break;
+      case 2: probe_hot<8, 2><<<grid, 256, 0, s>>>(B, H, idx, nidx, span, sink); break;
+      case 3: probe_hot<8, 3><<<grid, 256, 0, s>>>(B, H, idx, nidx, span, sink); break;
+      case 4: probe_hot<8, 4><<<grid, 256, 0, s>>>(B, H, idx, nidx, span, sink); break;
+      default: probe_hot<8, 0><<<grid, 256, 0, s>>>(B, H, idx, nidx, span, sink); break;
+    }
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 1 && ms < best) best = ms;
+  }
+  if (win_bytes > 0) {
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaCtxResetPersistingL2Cache();
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? best : -static_cast<float>(err);
+}
+
+extern "C" int64_t l2hot_max_persist(void) {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  return v;
+}
+
+// LDGSTS ring: D slots of U rows per warp in shared memory, rows copied with
+// 16-byte cp.async (a row of 32*VEC floats takes 8*VEC lanes; 32/(8*VEC) rows
+// per warp instruction), one commit group per slot, read back with one LDS per
+// lane per row.  MODE 1: cp.async.L2::cache_hint with evict_last (hot rows) /
+// evict_first (cold rows).
+template <int U, int D, int VEC, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    probe_ldgsts(const float* __restrict__ B, const int* __restrict__ idx, int64_t nidx, int span, int col0,
+                 float* sink) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int RB = 128 * VEC;          // row bytes
+  constexpr int LPR = RB / 16;           // lanes per row
+  constexpr int RPI = 32 / LPR;          // rows per warp instruction
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* ring = smraw + wib * (D * U * RB);
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t pl, pf;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  const int sub = lane / LPR, chunk = lane % LPR;
+  float a0 = 0.f;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    const int nb = static_cast<int>((s1 - s0 + U - 1) / U);
+    auto issue = [&](int k) {
+      if (k < nb) {
+        const int d = k % D;
+        const int64_t p0 = s0 + static_cast<int64_t>(k) * U;
+        const int my = (lane < U && p0 + lane < s1) ? __ldg(idx + p0 + lane) : 0;
+#pragma unroll
+        for (int u = 0; u < U; u += RPI) {
+          const int e = __shfl_sync(0xffffffffu, my, u + sub);
+          const bool hot = e < 0;
+          const uint32_t r = static_cast<uint32_t>(e) & 0x7fffffffu;
+          const float* src = B + static_cast<int64_t>(r) * 128 + col0 + 4 * chunk;
+          const uint32_t dst =
+              static_cast<uint32_t>(__cvta_generic_to_shared(ring + (d * U + u + sub) * RB + 16 * chunk));
+          if (MODE == 1) {
+            const uint64_t pol = hot ? pl : pf;
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                         "l"(pol) : "memory");
+          } else {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int k = 0; k < D - 1; ++k) issue(k);
+    for (int k = 0; k < nb; ++k) {
+      issue(k + D - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+      __syncwarp();
+      const int d = k % D;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float* row = reinterpret_cast<const float*>(ring + (d * U + u) * RB);
+        if (VEC == 4) {
+          const float4 v = reinterpret_cast<const float4*>(row)[lane];
+          a0 += v.x + v.y + v.z + v.w;
+        } else if (VEC == 2) {
+          const float2 v = reinterpret_cast<const float2*>(row)[lane];
+          a0 += v.x + v.y;
+        } else {
+          a0 += row[lane];
+        }
+      }
+      __syncwarp();
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  if (a0 == 1234.5f) sink[0] = a0;
+}
+
+extern "C" float l2hot_probe_ldgsts(const float* B, const int* idx, int64_t nidx, int mode, int vec, int U, int D,
+                                    int span, int warps_per_sm, int reps, float* sink, void* flush,
+                                    int64_t flush_bytes) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = 8 * D * U * 128 * vec;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  const int grid = sms * (warps_per_sm / 8);
+  const int w = 32 * vec;
+#define KB(UU, DD, VV, MM) probe_ldgsts<UU, DD, VV, MM>
+#define SETA(UU, DD, VV, MM) cudaFuncSetAttribute(KB(UU, DD, VV, MM), cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+#define RUN(UU, DD, VV, MM) KB(UU, DD, VV, MM)<<<grid, 256, smem>>>(B, idx, nidx, span, c0, sink)
+#define ALL(X, MM)                                          \
+  if (vec == 2 && U == 8 && D == 4) X(8, 4, 2, MM);        \
+  else if (vec == 2 && U == 8 && D == 3) X(8, 3, 2, MM);   \
+  else if (vec == 2 && U == 16 && D == 2) X(16, 2, 2, MM); \
+  else if (vec == 4 && U == 4 && D == 4) X(4, 4, 4, MM);   \
+  else if (vec == 4 && U == 8 && D == 2) X(8, 2, 4, MM);   \
+  else if (vec == 4 && U == 4 && D == 6) X(4, 6, 4, MM);   \
+  else X(8, 2, 2, MM);
+  if (mode == 1) { ALL(SETA, 1) } else { ALL(SETA, 0) }
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaDeviceSynchronize();
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    for (int c0 = 0; c0 < 128; c0 += w) {
+      if (mode == 1) { ALL(RUN, 1) } else { ALL(RUN, 0) }
+    }
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 1 && ms < best) best = ms;
+  }
+#undef ALL
+#undef RUN
+#undef SETA
+#undef KB
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? best : -static_cast<float>(err);
+}
