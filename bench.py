@@ -2,32 +2,42 @@
 "SpMM GFLOP/s (2*nnz*N) and achieved HBM GB/s vs roofline at 1/2/4/8 B200").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload config2|config1|config3-N|config4|config5] [--op sum|max|min|mean]
+                    [--workload config5|config2|config1|config3-N|config4] [--op sum|max|min|mean]
+                    [--scaling strong|weak] [--extra config2] [--b-panels P]
 
-Workload (default, BASELINE configs[1]): R-MAT scale 20 (1M rows), 16M edges
-requested (Graph500 a/b/c = .57/.19/.19, deduplicated), x dense B with N=64,
-fp32, sum-reduce.  Synthetic data, seeded; generated on the GPU.
+Workload (default): BASELINE configs[4], the north-star configuration -- R-MAT
+scale 24 (16M rows), 2^30 edges requested (Graph500 a/b/c = .57/.19/.19,
+deduplicated: 1.02 B nonzeros) x dense B with N=128, fp32, sum-reduce, on one
+GPU at N=1 and row-sharded (strong scaling) at N>1.  Synthetic, seeded,
+generated on the GPU with torch ops (workloads.rmat_csr) -- the SAME generator
+and seed in both arms, so the reference arm reads the identical matrix
+(``input`` carries a fingerprint in both lines).  configs[1] (R-MAT scale 20,
+N=64) rides along at N=1 under ``extra`` (kernel, roofline, e2e).
 
 A step = one execution of the hot path over the matrix with a cached plan
-(one kernel launch per column panel, after a reset of its item counter).  Each timed step is bracketed by CUDA events on the
-launching stream, with a 2x-L2 buffer written between steps (L2 flushed; the
-flush is outside the events).  N>1 (torchrun): row-block sharding, each rank
-runs its nnz-balanced row block after a one-time NCCL broadcast of B; time =
-max over ranks; value = total flops / that time ("strong" scaling).
+(one kernel launch per column panel, after a reset of its item counter).
+Each timed step is bracketed by CUDA events on the launching stream, with a
+2x-L2 buffer written between steps (L2 flushed; the flush is outside the
+events).  N>1 (torchrun): each rank owns an nnz-balanced row block; time = max
+over ranks.  Kernel-only steps run after B is on every rank; the
+broadcast-inclusive legs are reported separately (``broadcast``: B broadcast
+alone, broadcast then compute, and the column-panelled broadcast overlapped
+with the compute), and the N>1 ``e2e`` starts from pinned host buffers
+(root's B, every rank's CSR slab) and ends with every rank's C slab on the
+host.
 
 Extra keys: roofline (HBM, algorithmic compulsory bytes U per launch, the
-ncu DRAM traffic of the same kernel, and gather_ceiling: a live gather-only
-replay of the same column stream at the kernel's memory-level parallelism;
-see DESIGN.md), cpu_baseline (the oracle port on all host cores, ~10 s, plus a
-single-thread sample), e2e (host buffers through gespmm_csr_spmm_host:
-pipelined H2D + device colind check + plan + kernel + D2H), clocks (NVML
-samples inside the timed region; the nvidia-smi record rides along),
-sustained (the same steps after a 1 s soak at the power cap), c_allgather
-(N > 1: fused peer-store vs NCCL all-gather of C), gpu_launches.
+ncu DRAM traffic of the same kernel, and gather_ceiling at N=64), cpu_baseline
+(the oracle port on all host cores on a bounded row sample, plus one thread),
+e2e (N=1: host buffers through gespmm_csr_spmm_host -- pipelined H2D + device
+colind check + plan + kernel + D2H), clocks (NVML samples inside the timed
+region; the nvidia-smi record rides along), sustained (the same steps after a
+1 s soak at the power cap), c_allgather (N>1: fused peer-store vs NCCL
+all-gather of C), gpu_launches.
 
 --impl reference: the reference's own CPU implementation of the path (the
 unmodified raceset interpreter running gespmm_alg2.mir, oracle/_ref) on a
-bounded row sample of the same workload, all host threads, rank 0 only.
+bounded row sample of the same matrix, all host threads, rank 0 only.
 """
 from __future__ import annotations
 
@@ -45,15 +55,21 @@ sys.path.insert(0, ROOT)
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--workload", default="config5")
     ap.add_argument("--op", default="sum", choices=["sum", "max", "min", "mean"])
     ap.add_argument("--N", type=int, default=0, help="override the workload's dense width (sweeps)")
+    ap.add_argument("--extra", default="config2",
+                    help="N=1: comma-separated workloads measured after the headline one (kernel, roofline, "
+                         "e2e) and reported under 'extra'; '' = none")
+    ap.add_argument("--generator", default="torch", choices=["torch", "native"],
+                    help="R-MAT input: torch ops (both arms, identical matrix) or the library's CUDA "
+                         "generator (gespmm_rmat_csr)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
@@ -63,13 +79,15 @@ def parse_args():
                     help="soak length of the extra 'sustained' leg (0 = skip)")
     ap.add_argument("--variant", default="", help="kernel variant override (testing), e.g. vec1_lpr32_cwm2")
     ap.add_argument("--tile-work", type=int, default=0, help="plan tile size override (tuning); 0 = automatic")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = every rank owns one copy of the workload's rows (the job is N "
-                         "row-stacked copies sharing B: per-GPU work fixed); strong = the workload's "
-                         "rows split across ranks (nnz-balanced)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the workload's rows split nnz-balanced across ranks (default, "
+                         "the north-star run); weak = every rank owns one copy of the workload's rows "
+                         "(the job is N row-stacked copies sharing B)")
+    ap.add_argument("--b-panels", type=int, default=4,
+                    help="N > 1: column panels of the B broadcast overlapped with the compute")
     ap.add_argument("--ref-sample-products", type=int, default=800_000,
                     help="--impl reference: nnz*N products per step (bounds interpreter RAM)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def peaks():
@@ -90,7 +108,7 @@ def workload_spec(name):
                     desc="R-MAT scale 22 (4M rows), 64M edges requested (dedup), N=128 (configs[3])")
     if name == "config5":
         return dict(kind="rmat", scale=24, edges=2**30, N=128, seed=3,
-                    desc="R-MAT scale 24 (16M rows), 2^30 edges requested (dedup), N=128 (configs[4], one GPU)")
+                    desc="R-MAT scale 24 (16M rows), 2^30 edges requested (dedup), N=128 (configs[4])")
     if name == "config1":
         return dict(kind="uniform", M=4096, K=4096, density=0.01, N=32, seed=1,
                     desc="uniform 4096x4096, 1% density, N=32 (configs[0])")
@@ -101,18 +119,18 @@ def workload_spec(name):
     raise SystemExit(f"unknown workload {name}")
 
 
-def make_workload(spec, device, native=True):
-    """native=True: the library's CUDA generators (gespmm_rmat_csr /
-    gespmm_uniform_fill); the reference arm passes native=False and gets the
-    same recursion from torch ops, so no libgespmm code runs on that arm."""
-    import numpy as np
+def make_workload(spec, device, generator="torch"):
+    """R-MAT: generator="torch" builds the matrix and B with torch ops
+    (workloads.rmat_csr / dense_torch) -- what BOTH arms use by default, so the
+    reference arm reads the identical input and no libgespmm code runs on its
+    path; "native" uses the library's CUDA generators (gespmm_rmat_csr:
+    Philox keys + CUB sort/unique; a different graph of the same law)."""
     import torch
 
     from paper_2503_08946_b200 import workloads as W
 
-    native = native and device.type == "cuda"
+    native = generator == "native" and device.type == "cuda"
     if spec["kind"] == "rmat" and native:
-        # native CUDA generator (gespmm_rmat_csr: Philox keys, CUB sort + unique)
         csr = W.rmat_csr_gpu(spec["scale"], spec["edges"], seed=spec["seed"], device=device)
     elif spec["kind"] == "rmat":
         csr = W.rmat_csr(spec["scale"], spec["edges"], seed=spec["seed"], device=device)
@@ -126,8 +144,18 @@ def make_workload(spec, device, native=True):
         B = W.dense_gpu(csr.K, spec["N"], seed=2, device=device)
     else:
         B = W.dense_torch(csr.K, spec["N"], seed=2, device=device)
-    del np
     return csr, B
+
+
+def fingerprint(csr, B):
+    """Identity of the input, printed by both arms (same numbers = same matrix)."""
+    import torch
+
+    return {"M": int(csr.M), "K": int(csr.K), "nnz": int(csr.nnz), "N": int(B.shape[1]),
+            "sum_rowptr": int(csr.rowptr.to(torch.int64).sum()),
+            "sum_colind": int(csr.colind.to(torch.int64).sum()),
+            "sum_vals": round(float(csr.vals.to(torch.float64).sum()), 6),
+            "sum_B": round(float(B.to(torch.float64).sum()), 6)}
 
 
 def algorithmic_bytes(M, K, N, nnz):
@@ -238,43 +266,63 @@ class NvmlSampler:
                 "samples": len(self.sm), "window": window, "source": "NVML, ~2 ms"}
 
 
-def cpu_baseline_port(csr, B, N, budget_s=10.0):
+def row_sample(rp, target_nnz):
+    """Every s-th row (s chosen so the sample holds ~target_nnz nonzeros): a
+    bounded sample that keeps the matrix's degree mix (R-MAT's heavy rows
+    are spread over the whole row range, not front-loaded)."""
+    import numpy as np
+
+    nnz = int(rp[-1])
+    M = rp.shape[0] - 1
+    s = max(1, -(-nnz // max(1, target_nnz)))
+    rows = np.arange(0, M, s, dtype=np.int64)
+    deg = (rp[rows + 1] - rp[rows]).astype(np.int64)
+    srp = np.zeros(rows.size + 1, np.int64)
+    srp[1:] = np.cumsum(deg)
+    starts = rp[rows].astype(np.int64)
+    pos = np.repeat(starts - srp[:-1], deg) + np.arange(int(srp[-1]), dtype=np.int64)
+    return rows, srp.astype(np.int32), pos, s
+
+
+def cpu_baseline_port(rp, ci, vv, Bh, N, op, budget_s=10.0, target_nnz=64 << 20):
     """The oracle's fp32 restatement (oracle/gespmm_oracle.c, OpenMP, all host
-    threads) on the full matrix, repeated for ~budget_s (about 10 s of CPU
-    work, the contract's bounded sample); best run."""
+    threads) on a bounded sample of the same matrix (the whole matrix when it
+    has <= target_nnz nonzeros, else every s-th row against the full B),
+    repeated for ~budget_s (the contract's 10-30 s of CPU work); best run.
+    Plus one host thread on a 2M-nonzero block."""
     import numpy as np
 
     from oracle import oracle as O
 
-    rp = csr.rowptr.cpu().numpy()
-    ci = csr.colind.cpu().numpy()
-    vv = csr.vals.cpu().numpy()
-    Bh = np.ascontiguousarray(B.cpu().numpy())
     nth = O.num_threads()
-    best = None
+    if int(rp[-1]) > target_nnz:
+        rows, srp, pos, s = row_sample(rp, target_nnz)
+        sci, svv = ci[pos], vv[pos]
+        what = f"every {s}th row ({rows.size} rows, {int(srp[-1])} nnz) of the same matrix x the full B"
+    else:
+        srp, sci, svv = rp, ci, vv
+        what = f"full workload (M={rp.shape[0] - 1}, nnz={int(rp[-1])})"
+    best, runs = None, 0
     t_end = time.perf_counter() + budget_s
-    runs = 0
     while True:
         t0 = time.perf_counter()
-        O.spmm_f32(rp, ci, vv, Bh, "sum", seg_len=256, nthreads=nth)
+        O.spmm_f32(srp, sci, svv, Bh, op, seg_len=256, nthreads=nth)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
         runs += 1
         if time.perf_counter() > t_end or runs >= 400:
             break
-    gflops = 2.0 * csr.nnz * N / best / 1e9
-    # single host thread on a bounded row block (SURVEY.md 8(d): 1 thread and nproc threads)
-    r1 = min(csr.M, int(np.searchsorted(rp, min(int(rp[-1]), 2_000_000))) + 1)
-    rp1 = rp[:r1 + 1]
-    p1 = int(rp1[-1])
+    gflops = 2.0 * int(srp[-1]) * N / best / 1e9
+    r1 = min(srp.shape[0] - 1, int(np.searchsorted(srp, min(int(srp[-1]), 2_000_000))) + 1)
+    p1 = int(srp[r1])
     t0 = time.perf_counter()
-    O.spmm_f32(rp1, ci[:p1], vv[:p1], Bh, "sum", seg_len=256, nthreads=1)
+    O.spmm_f32(srp[:r1 + 1], sci[:p1], svv[:p1], Bh, op, seg_len=256, nthreads=1)
     dt1 = time.perf_counter() - t0
     return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": nth, "kind": "port",
-            "sample": f"full workload (M={csr.M}, nnz={csr.nnz}, N={N}), best of {runs} runs in ~{budget_s:.0f} s, "
+            "sample": f"{what}, N={N}, {op}; best of {runs} runs in ~{budget_s:.0f} s; "
                       f"oracle/gespmm_oracle.c fp32 twin, OpenMP {nth} threads",
             "single_thread": {"value": round(2.0 * p1 * N / dt1 / 1e9, 3), "unit": "GFLOP/s", "cores": 1,
-                              "sample": f"first {r1} rows ({p1} nnz) of the same matrix, one run"}}
+                              "sample": f"first {r1} rows ({p1} nnz) of that sample, one run"}}
 
 
 def time_allgather(plan, vals, B, C, bounds, rank, world, op, stream, dev, reps=5):
@@ -299,22 +347,6 @@ def time_allgather(plan, vals, B, C, bounds, rank, world, op, stream, dev, reps=
             opened.append(base)
             peers.append(base + ow)
 
-    def timed(fn):
-        ts = []
-        for _ in range(reps + 1):
-            torch.cuda.synchronize()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            fn()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            dist.barrier()  # every rank's peer stores have landed
-            ts.append(e0.elapsed_time(e1))
-        t = torch.tensor([sum(ts[1:]) / reps], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     def fused():
         plan.execute_peers(vals, B, full_f[a:b], peers, a, reduce=op, stream=stream)
 
@@ -325,19 +357,48 @@ def time_allgather(plan, vals, B, C, bounds, rank, world, op, stream, dev, reps=
             if hi > lo:
                 dist.broadcast(full_n[lo:hi], src=w)
 
-    t_f = timed(fused)
-    t_n = timed(nccl)
+    t_f = timed_region(fused, stream, dev, world, reps)
+    t_n = timed_region(nccl, stream, dev, world, reps)
     same = bool(torch.equal(full_f, full_n))
     for base in opened:
         ipc_close(base)
+    del full_f, full_n
     return {"fused_peer_stores_ms": t_f, "nccl_broadcasts_ms": t_n, "identical": same,
             "bytes_per_rank": int((b - a) * N * 4 * (world - 1)),
             "what": "compute + full C on every rank; fused = kernel epilogue stores into every "
                     "rank's full C over NVLink (CUDA IPC), nccl = execute then one broadcast per slab owner"}
 
 
+def timed_region(fn, stream, dev, world, reps=5, before=None):
+    """Mean device time of fn() over reps (after one untimed run), CUDA events
+    on `stream`, barrier + synchronize on both sides, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    ts = []
+    for _ in range(reps + 1):
+        if before is not None:
+            before()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ts.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(ts[1:]) / reps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_reference(args):
-    """Reference arm: the unmodified reference interpreter (oracle/_ref)."""
+    """Reference arm: the unmodified reference interpreter (oracle/_ref) on
+    the identical matrix (same torch generator and seed as our arm)."""
     import numpy as np
     import torch
 
@@ -348,26 +409,33 @@ def run_reference(args):
     from oracle import oracle as O
 
     spec = workload_spec(args.workload)
+    if args.N > 0:
+        spec["N"] = args.N
     if not O.ref_available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libgespmm_ref.so not built (reference tree absent at build time)"}))
         return 0
     dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
-    csr, B = make_workload(spec, dev, native=False)
+    csr, B = make_workload(spec, dev, "torch")
+    fp = fingerprint(csr, B)
     N = spec["N"]
     rp = csr.rowptr.cpu().numpy().astype(np.int64)
     ci = csr.colind.cpu().numpy()
     vv = csr.vals.cpu().numpy()
     Bh = np.ascontiguousarray(B.cpu().numpy())
+    del csr, B
     nth = os.cpu_count() or 1
     target_nnz = max(1, args.ref_sample_products // N)
-    M = csr.M
+    M = rp.shape[0] - 1
     deg = np.diff(rp)
-    cap = max(1, target_nnz // nth)  # longer rows would leave host threads idle
+    # the interpreter runs one instance per host thread; a row longer than
+    # target/threads would leave the other threads idle (and a 10^5-nonzero row
+    # takes the interpreter minutes), so the sample draws from rows up to `cap`
+    cap = max(1, target_nnz // nth)
 
     def sample(i):
         """Rows drawn uniformly at random (seeded per step) until ~target_nnz
-        nonzeros; rows longer than target/threads are skipped."""
+        nonzeros; rows longer than cap are skipped (recorded in the line)."""
         order = np.random.default_rng(1000 + i).permutation(M)
         d = deg[order]
         ok = order[(d > 0) & (d <= cap)]
@@ -392,12 +460,17 @@ def run_reference(args):
         tot_s += s
         tot_rows += rows
     value = 2.0 * tot_nnz * N / tot_s / 1e9
+    skipped = deg > cap
     line = {
         "metric": "SpMM GFLOP/s (2*nnz*N)", "value": value, "unit": "GFLOP/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_s / max(args.steps, 1) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": spec["desc"], "op": "sum", "N": N, "M": M, "nnz": csr.nnz},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": spec["desc"], "op": "sum", "N": N, "M": M, "nnz": int(rp[-1]),
+                   "input": fp, "generator": "torch ops (workloads.rmat_csr), same seed as the GPU arm",
+                   "sample": {"nnz_per_step": target_nnz, "row_cap_nnz": cap,
+                              "rows_over_cap": int(skipped.sum()),
+                              "nnz_in_rows_over_cap": int(deg[skipped].sum())}},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": nth, "kind": "reference",
                          "sample": f"per step ~{target_nnz} nnz in {tot_rows / max(args.steps, 1):.0f} "
                                    f"rows drawn at random (seeded; rows > {cap} nnz skipped) from "
@@ -410,17 +483,338 @@ def run_reference(args):
     return 0
 
 
+def ncu_record(name, workload, op, world):
+    """The committed ncu capture of the same kernel and workload (profiles/):
+    DRAM bytes per launch (traffic.json) and the ncu metric summary."""
+    if world != 1:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f).get(f"{workload}:{op}")
+    except Exception:
+        return None
+
+
+def pinned_like(t):
+    import torch
+
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h
+
+
+class Measure:
+    """One workload on this rank: build, plan, timed steps and the legs."""
+
+    def __init__(self, args, name, dev, world, rank, local):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        from paper_2503_08946_b200.spmm import Plan, partition_rows
+
+        self.args, self.name, self.dev, self.world, self.rank = args, name, dev, world, rank
+        spec = workload_spec(name)
+        if args.N > 0 and name == args.workload:
+            spec["N"] = args.N
+            spec["desc"] += f" [N overridden to {args.N}]"
+        self.spec = spec
+        self.N = N = spec["N"]
+        csr, B = make_workload(spec, dev, args.generator)
+        self.fp = fingerprint(csr, B)
+        self.K = K = csr.K
+        self.stream = stream = torch.cuda.current_stream(dev)
+        self.M_all, self.nnz_all = csr.M, csr.nnz
+        if world > 1 and args.scaling == "weak":
+            # the job is `world` row-stacked copies of the workload's rows, all
+            # gathering from one B; rank r owns rows [rM, (r+1)M)
+            self.bounds = np.arange(world + 1, dtype=np.int64) * csr.M
+            rowptr, colind, vals = csr.rowptr, csr.colind, csr.vals
+            self.M_all, self.nnz_all = csr.M * world, csr.nnz * world
+        elif world > 1:
+            rp_h = csr.rowptr.cpu().numpy()
+            self.bounds = partition_rows(rp_h, world)
+            a, b = int(self.bounds[rank]), int(self.bounds[rank + 1])
+            p0, p1 = int(rp_h[a]), int(rp_h[b])
+            rowptr = (csr.rowptr[a:b + 1] - p0).contiguous()
+            colind = csr.colind[p0:p1].contiguous()
+            vals = csr.vals[p0:p1].contiguous()
+            del rp_h
+        else:
+            self.bounds = None
+            rowptr, colind, vals = csr.rowptr, csr.colind, csr.vals
+        del csr
+        self.B_root = None
+        if world > 1:
+            if rank == 0:
+                self.B_root = B.clone()  # the root's copy survives the broadcast legs
+            else:
+                B.zero_()  # only the root holds B; the broadcast is the exchange step
+            torch.cuda.synchronize()
+            dist.barrier()
+            self.bcast_ms = timed_region(lambda: dist.broadcast(B, src=0), stream, dev, world, reps=3)
+        else:
+            self.bcast_ms = 0.0
+        self.rowptr, self.colind, self.vals, self.B = rowptr, colind, vals, B
+        self.M_loc, self.nnz_loc = rowptr.numel() - 1, colind.numel()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        self.plan = Plan(rowptr, colind, K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        self.plan_ms = e0.elapsed_time(e1)
+        self.plan_wall_ms = (time.perf_counter() - t0) * 1e3
+        self.info = self.plan.info()
+        self.C = torch.empty((self.M_loc, N), dtype=torch.float32, device=dev)
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        self.flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+
+    def run_once(self):
+        self.plan.execute(self.vals, self.B, self.args.op, out=self.C, stream=self.stream)
+
+    def steps(self, n, warmup):
+        import torch
+        import torch.distributed as dist
+
+        for _ in range(max(warmup, 3)):
+            self.flush.zero_()
+            self.run_once()
+        torch.cuda.synchronize()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(n):
+            self.flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[i].record(self.stream)
+            self.run_once()
+            ends[i].record(self.stream)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        return [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+
+    def soak(self, seconds):  # back-to-back launches (sustained load)
+        import torch
+
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end:
+            for _ in range(50 if self.N * self.nnz_loc < 1 << 32 else 4):
+                self.run_once()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(self, ms):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=self.dev, dtype=torch.float64)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def roofline(self, t_mean):
+        U, G = algorithmic_bytes(self.M_loc, self.K, self.N, self.nnz_loc)
+        peak, peak_src = peaks()
+        achieved = U / (t_mean * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": ncu_record("traffic.json", self.name, self.args.op, self.world),
+                "bytes_model": f"U = 4(M+1) + 8nnz + 4KN + 4MN = {U} B per launch",
+                "peak_source": peak_src, "gather_bytes_G": G, "gather_GBs": G / (t_mean * 1e-3) / 1e9,
+                "ncu": ncu_record("ncu_metrics.json", self.name, self.args.op, self.world)}
+
+    def gather_ceiling(self, t_mean):
+        """tools/gather_probe.cu replays this matrix's colind as B-row gathers
+        at the kernel's memory-level parallelism (8 loads/warp, 32 warps/SM,
+        256-nonzero spans) with nothing else: the floor for any kernel
+        gathering the same rows in the same order.  N=64."""
+        import ctypes
+
+        import torch
+
+        probe = os.path.join(ROOT, "tools", "libgather_probe.so")
+        if self.N != 64 or self.world != 1 or not os.path.exists(probe) or os.environ.get("GESPMM_NO_PROBE"):
+            return None
+        Lp = ctypes.CDLL(probe)
+        Lp.gather_probe.restype = ctypes.c_float
+        Lp.gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_int64]
+        sink = torch.zeros(4, device=self.dev)
+        args = (self.B.data_ptr(), self.colind.data_ptr(), self.nnz_loc)
+        pms = Lp.gather_probe(*args, 8, 256, 4, 5, sink.data_ptr(), self.flush.data_ptr(), self.flush.numel() * 4)
+        pms16 = Lp.gather_probe(*args, 16, 256, 4, 5, sink.data_ptr(), self.flush.data_ptr(),
+                                self.flush.numel() * 4)
+        if pms <= 0:
+            return None
+        return {"probe_ms": pms, "kernel_ms": t_mean, "frac": pms / t_mean, "probe_ms_16_in_flight": pms16,
+                "what": "gather-only replay of this colind stream, 8 loads/warp x 32 warps/SM "
+                        "(tools/gather_probe.cu, best of 5, L2 flushed)"}
+
+    def e2e_single(self, flops, reps):
+        """N=1: the public host entry point (gespmm_csr_spmm_host) on pinned
+        host buffers, wall clock per call."""
+        import torch
+
+        from paper_2503_08946_b200.spmm import csr_spmm_host
+
+        h_rp, h_ci, h_v, h_B = (pinned_like(t) for t in (self.rowptr, self.colind, self.vals, self.B))
+        h_C = torch.empty((self.M_loc, self.N), dtype=torch.float32, pin_memory=True)
+        csr_spmm_host(h_rp, h_ci, h_v, h_B, self.args.op, out=h_C)  # warm
+        et = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            csr_spmm_host(h_rp, h_ci, h_v, h_B, self.args.op, out=h_C)
+            et.append(time.perf_counter() - t0)
+        ok = bool(torch.equal(h_C, self.C.cpu()))
+        self.host = (h_rp, h_ci, h_v, h_B)
+        t = statistics.median(et)
+        return {"value": flops / t / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(4 * (self.M_loc + 1) + 8 * self.nnz_loc + 4 * self.K * self.N),
+                "d2h_bytes_per_step": int(4 * self.M_loc * self.N),
+                "ms_per_step": t * 1e3, "reps": reps, "stat": "median", "equals_device_result": ok,
+                "path": "gespmm_csr_spmm_host (pinned host buffers; pipelined: rowptr + B H2D, "
+                        "plan, then per item-aligned row chunk, fewest nonzeros first: colind/vals "
+                        "H2D -> device colind check -> kernel -> C rows D2H overlapping the next "
+                        "chunk; wall clock per call)"}
+
+    def broadcast_legs(self, panels):
+        """N>1: the exchange step with the compute -- B broadcast alone,
+        broadcast then compute, and the column-panelled broadcast overlapped
+        with the compute (sharded.broadcast_B_overlapped); device time on the
+        compute stream, max over ranks.  B is re-zeroed on non-root ranks
+        before every repetition, so each one really moves B."""
+        import torch
+        import torch.distributed as dist
+
+        from paper_2503_08946_b200 import sharded as S
+
+        B, st, world, rank = self.B, self.stream, self.world, self.rank
+        comm = torch.cuda.Stream(device=self.dev)
+        C2 = torch.empty_like(self.C)
+        packed = [torch.empty((self.K, c1 - c0), dtype=torch.float32, device=self.dev)
+                  for c0, c1 in S.panel_bounds(self.N, panels)]
+
+        def reset():
+            if rank != 0:
+                B.zero_()
+                for t in packed:
+                    t.zero_()
+            else:
+                B.copy_(self.B_root)
+
+        def serial():
+            dist.broadcast(B, src=0)
+            self.plan.execute(self.vals, B, self.args.op, out=self.C, stream=st)
+
+        def overlapped():
+            def panel(p, Bp, c0, c1):
+                self.plan.execute(self.vals, Bp, self.args.op, out=C2[:, c0:c1], stream=st)
+            S.broadcast_B_overlapped(panel, B, panels, 0, None, cuda_streams=(st, comm), packed=packed)
+
+        t_ser = timed_region(serial, st, self.dev, world, reps=3, before=reset)
+        t_ovl = timed_region(overlapped, st, self.dev, world, reps=3, before=reset)
+        same = bool(torch.equal(C2, self.C))
+        ident = torch.tensor([1 if same else 0], device=self.dev)
+        dist.all_reduce(ident, op=dist.ReduceOp.MIN)
+        reset()
+        dist.broadcast(B, src=0)  # leave B complete on every rank
+        torch.cuda.synchronize()
+        del C2, packed
+        return {"b_broadcast_ms": self.bcast_ms, "broadcast_then_compute_ms": t_ser,
+                "overlapped_ms": t_ovl, "b_panels": len(S.panel_bounds(self.N, panels)),
+                "identical": bool(ident.item()), "b_bytes": int(self.K * self.N * 4),
+                "what": "device time on the compute stream, max over ranks; overlapped = B cut into column "
+                        "panels, panel p broadcast (NCCL, comm stream) while panel p-1 computes"}
+
+    def e2e_sharded(self, flops, panels, reps):
+        """N>1 end to end: pinned host buffers (the root's B, every rank's CSR
+        slab) -> H2D -> plan -> column-panelled B broadcast overlapped with the
+        compute -> this rank's C slab D2H; wall clock, max over ranks."""
+        import torch
+        import torch.distributed as dist
+
+        from paper_2503_08946_b200 import sharded as S
+        from paper_2503_08946_b200.spmm import Plan
+
+        dev, st = self.dev, self.stream
+        h_rp, h_ci, h_v = (pinned_like(t) for t in (self.rowptr, self.colind, self.vals))
+        h_B = pinned_like(self.B_root) if self.rank == 0 else None
+        h_C = torch.empty((self.M_loc, self.N), dtype=torch.float32, pin_memory=True)
+        d_B = torch.zeros((self.K, self.N), dtype=torch.float32, device=dev)
+        d_C = torch.empty_like(self.C)
+        comm = torch.cuda.Stream(device=dev)
+        packed = [torch.empty((self.K, c1 - c0), dtype=torch.float32, device=dev)
+                  for c0, c1 in S.panel_bounds(self.N, panels)]
+
+        def call():
+            rp, ci, v = (h.to(dev, non_blocking=True) for h in (h_rp, h_ci, h_v))
+            if h_B is not None:
+                d_B.copy_(h_B, non_blocking=True)
+            plan = Plan(rp, ci, self.K)
+
+            def panel(p, Bp, c0, c1):
+                plan.execute(v, Bp, self.args.op, out=d_C[:, c0:c1], stream=st)
+            S.broadcast_B_overlapped(panel, d_B, panels, 0, None, cuda_streams=(st, comm), packed=packed)
+            h_C.copy_(d_C, non_blocking=True)
+            torch.cuda.synchronize()
+            plan.close()
+
+        call()
+        et = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            call()
+            et.append(time.perf_counter() - t0)
+        t = self.max_over_ranks(statistics.median(et))
+        ok = bool(torch.equal(h_C, self.C.cpu()))
+        ident = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(ident, op=dist.ReduceOp.MIN)
+        n_pan = len(packed)
+        del d_B, d_C, packed
+        return {"value": flops / t / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(4 * (self.M_loc + 1) + 8 * self.nnz_loc
+                                          + (4 * self.K * self.N if self.rank == 0 else 0)),
+                "d2h_bytes_per_step": int(4 * self.M_loc * self.N), "bytes_are": "rank 0's",
+                "ms_per_step": t * 1e3, "reps": reps, "stat": "median, max over ranks",
+                "equals_device_result": bool(ident.item()), "b_panels": n_pan,
+                "path": "pinned host CSR slab per rank + root's B -> H2D -> Plan -> column-panelled NCCL "
+                        "B broadcast overlapped with the compute -> C slab D2H; wall clock"}
+
+
+def measure_extra(args, name, dev):
+    """A secondary workload at N=1: kernel steps, roofline, gather ceiling, e2e."""
+    import torch
+
+    m = Measure(args, name, dev, 1, 0, 0)
+    times = m.steps(args.steps, args.warmup)
+    t = sum(times) / len(times)
+    flops = 2.0 * m.nnz_all * m.N
+    out = {"workload": m.spec["desc"], "op": args.op, "N": m.N, "nnz": m.nnz_all, "input": m.fp,
+           "value": flops / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
+           "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
+           "roofline": m.roofline(t), "gather_ceiling": m.gather_ceiling(t)}
+    if not args.no_e2e:
+        out["e2e"] = m.e2e_single(flops, reps=max(3, min(args.steps, 10)))
+    del m
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2503_08946_b200.spmm import (Plan, csr_spmm_host, partition_rows, set_variant_override,
-                                            variant_name)
+    from paper_2503_08946_b200.spmm import panel_width, set_variant_override, variant_name
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -437,128 +831,29 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-
-    spec = workload_spec(args.workload)
-    if args.N > 0:
-        spec["N"] = args.N
-        spec["desc"] += f" [N overridden to {args.N}]"
-    N = spec["N"]
     if args.variant:
         set_variant_override(args.variant)
     if args.tile_work:
         from paper_2503_08946_b200.spmm import set_tile_work_override
         set_tile_work_override(args.tile_work)
-    csr, B = make_workload(spec, dev)
-    M_all, K, nnz_all = csr.M, csr.K, csr.nnz
-    stream = torch.cuda.current_stream(dev)
 
-    # ---- row-block sharding (world > 1) ----------------------------------
-    # weak: the job is `world` row-stacked copies of the workload's rows, all
-    # gathering from one B (A_job = [A; A; ...], C_job = [C; C; ...]); rank r
-    # owns rows [r*M, (r+1)*M) -- per-GPU work equals the 1-GPU run.
-    # strong: the workload's own rows split nnz-balanced across ranks.
-    if world > 1 and args.scaling == "weak":
-        bounds = np.arange(world + 1, dtype=np.int64) * M_all
-        rowptr, colind, vals = csr.rowptr, csr.colind, csr.vals
-        M_all, nnz_all = M_all * world, nnz_all * world
-        if rank != 0:
-            B.zero_()  # only the root holds B; the broadcast is the exchange step
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        dist.broadcast(B, src=0)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        bcast_ms = e0.elapsed_time(e1)
-    elif world > 1:
-        rp_h = csr.rowptr.cpu().numpy()
-        bounds = partition_rows(rp_h, world)
-        a, b = int(bounds[rank]), int(bounds[rank + 1])
-        p0, p1 = int(rp_h[a]), int(rp_h[b])
-        rowptr = (csr.rowptr[a:b + 1] - p0).contiguous()
-        colind = csr.colind[p0:p1].contiguous()
-        vals = csr.vals[p0:p1].contiguous()
-        if rank != 0:
-            B.zero_()  # only the root holds B; the broadcast is the exchange step
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        dist.broadcast(B, src=0)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        bcast_ms = e0.elapsed_time(e1)
-    else:
-        rowptr, colind, vals = csr.rowptr, csr.colind, csr.vals
-        bcast_ms = 0.0
-    M_loc, nnz_loc = rowptr.numel() - 1, colind.numel()
-
-    # ---- plan (cached across steps; its build is reported separately) ----
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    e0.record(stream)
-    plan = Plan(rowptr, colind, K)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    plan_ms = e0.elapsed_time(e1)
-    plan_wall_ms = (time.perf_counter() - t0) * 1e3
-    info = plan.info()
-    C = torch.empty((M_loc, N), dtype=torch.float32, device=dev)
-
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
-
-    def run_once():
-        plan.execute(vals, B, args.op, out=C, stream=stream)
-
-    for _ in range(max(args.warmup, 3)):
-        flush.zero_()
-        run_once()
-    torch.cuda.synchronize()
-
+    m = Measure(args, args.workload, dev, world, rank, local)
+    N, K = m.N, m.K
     clocks = ClockSampler(local, enabled=not args.no_clocks and rank == 0)
     nvml = NvmlSampler(local, enabled=not args.no_clocks and rank == 0)
-
-    def soak(seconds):  # back-to-back launches (sustained load)
-        t_end_soak = time.perf_counter() + seconds
-        while time.perf_counter() < t_end_soak:
-            for _ in range(50):
-                run_once()
-            torch.cuda.synchronize()
-
-    def timed_steps():
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            starts[i].record(stream)
-            run_once()
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        return [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
-
-    soak(args.soak_s)
+    m.soak(args.soak_s)
     nvml.start()
-    times = timed_steps()
+    times = m.steps(args.steps, args.warmup)
     clk_nvml = nvml.stop("timed region")
-    # sustained: the same steps after ~1 s of back-to-back launches (the part
-    # reaches its power cap; clocks sampled over soak + steps)
     sustained = None
     if args.sustained_s > 0:
+        # the same steps after ~1 s of back-to-back launches (the part reaches
+        # its power cap; clocks sampled over soak + steps)
         nvml2 = NvmlSampler(local, enabled=not args.no_clocks and rank == 0)
         nvml2.start()
-        soak(args.sustained_s)
-        times2 = timed_steps()
-        t2 = torch.tensor([sum(times2) / len(times2)], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        sustained = {"ms_per_step": float(t2.item()), "soak_s": args.sustained_s,
+        m.soak(args.sustained_s)
+        times2 = m.steps(args.steps, 0)
+        sustained = {"ms_per_step": m.max_over_ranks(sum(times2) / len(times2)), "soak_s": args.sustained_s,
                      "clocks": nvml2.stop(f"{args.sustained_s} s soak + timed steps")}
     clk = clocks.stop()
     if clk is not None:
@@ -567,144 +862,82 @@ def main():
         clk_nvml["nvidia_smi"] = clk
         clk = clk_nvml
     t_mean = sum(times) / len(times)
-    t_max = torch.tensor([t_mean], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    t_job = float(t_max.item())  # ms, max over ranks
-
-    from paper_2503_08946_b200.spmm import panel_width
+    t_job = m.max_over_ranks(t_mean)  # ms, max over ranks
     pw = panel_width(K, N)
     n_panels = (N + pw - 1) // pw
-    flops = 2.0 * nnz_all * N
+    flops = 2.0 * m.nnz_all * N
     value = flops / (t_job * 1e-3) / 1e9
-    U, G = algorithmic_bytes(M_loc, K, N, nnz_loc)
-    peak, peak_src = peaks()
-    achieved = U / (t_mean * 1e-3) / 1e9
+    roof = m.roofline(t_mean)
+    roof["gather_ceiling"] = m.gather_ceiling(t_mean)
 
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath) and world == 1:  # ncu bytes of the single-GPU launch
-        try:
-            with open(tpath) as f:
-                traffic = json.load(f).get(f"{args.workload}:{args.op}")
-        except Exception:
-            traffic = None
-    # the >= 70 % HBM target is stated on ncu DRAM throughput, with
-    # the L2 sector hit rate beside it -- from the committed capture of the
-    # same kernel and workload (never measured under ncu here)
-    ncu = None
-    npath = os.path.join(ROOT, "profiles", "ncu_metrics.json")
-    if os.path.exists(npath) and world == 1:
-        try:
-            with open(npath) as f:
-                ncu = json.load(f).get(f"{args.workload}:{args.op}")
-        except Exception:
-            ncu = None
-
-    # ---- C all-gather (N > 1): fused peer stores vs NCCL after the compute --
-    # The fused path (gespmm_plan_execute_peers) writes every finished C row
-    # into every rank's full-C buffer over NVLink from the kernel epilogue
-    # (CUDA IPC); the baseline computes the slab, then one NCCL broadcast per
-    # slab owner.  Both timed on the device, max over ranks.
     c_allgather = None
     if world > 1 and not args.no_allgather:
         try:
-            c_allgather = time_allgather(plan, vals, B, C, bounds, rank, world, args.op, stream, dev)
+            c_allgather = time_allgather(m.plan, m.vals, m.B, m.C, m.bounds, rank, world, args.op, m.stream, dev)
         except Exception as ex:  # report, never fail the bench line
             c_allgather = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    broadcast = None
+    if world > 1:
+        broadcast = m.broadcast_legs(args.b_panels)
 
-    # ---- live gather ceiling: the same column stream, gathers only ---------
-    # tools/gather_probe.cu replays this matrix's colind as B-row gathers at the
-    # kernel's memory-level parallelism (8 loads/warp, 32 warps/SM, 256-nonzero
-    # spans) with nothing else; its time is the floor for any kernel gathering
-    # the same rows in the same order.  N = 64 only.
-    gather_ceiling = None
-    probe = os.path.join(ROOT, "tools", "libgather_probe.so")
-    if N == 64 and world == 1 and os.path.exists(probe) and not os.environ.get("GESPMM_NO_PROBE"):
-        import ctypes
-
-        Lp = ctypes.CDLL(probe)
-        Lp.gather_probe.restype = ctypes.c_float
-        Lp.gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
-                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
-                                    ctypes.c_void_p, ctypes.c_int64]
-        sink = torch.zeros(4, device=dev)
-        pms = Lp.gather_probe(B.data_ptr(), colind.data_ptr(), nnz_loc, 8, 256, 4, 5, sink.data_ptr(),
-                              flush.data_ptr(), flush.numel() * 4)
-        pms16 = Lp.gather_probe(B.data_ptr(), colind.data_ptr(), nnz_loc, 16, 256, 4, 5, sink.data_ptr(),
-                                flush.data_ptr(), flush.numel() * 4)
-        if pms > 0:
-            gather_ceiling = {"probe_ms": pms, "kernel_ms": t_mean, "frac": pms / t_mean,
-                              "probe_ms_16_in_flight": pms16,
-                              "what": "gather-only replay of this colind stream, 8 loads/warp x 32 warps/SM "
-                                      "(tools/gather_probe.cu, best of 5, L2 flushed)"}
-
-    # ---- e2e through the public host API (H2D + validate + plan + kernel + D2H)
     e2e = None
     if not args.no_e2e:
-        hp = lambda t: t.cpu().pin_memory()  # noqa: E731
-        h_rp, h_ci, h_v, h_B = hp(rowptr), hp(colind), hp(vals), hp(B)
-        h_C = torch.empty((M_loc, N), dtype=torch.float32).pin_memory()
-        csr_spmm_host(h_rp, h_ci, h_v, h_B, args.op, out=h_C)  # warm
         reps = max(3, min(args.steps, 10))
-        et = []
-        for _ in range(reps):
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            csr_spmm_host(h_rp, h_ci, h_v, h_B, args.op, out=h_C)
-            et.append(time.perf_counter() - t0)
-        e2e_t = torch.tensor([sum(et) / len(et)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        e2e = {"value": flops / float(e2e_t.item()) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(4 * (M_loc + 1) + 8 * nnz_loc + 4 * K * N),
-               "d2h_bytes_per_step": int(4 * M_loc * N),
-               "ms_per_step": float(e2e_t.item()) * 1e3,
-               "path": "gespmm_csr_spmm_host (pinned host buffers; pipelined: rowptr + B H2D, "
-                       "plan, then per item-aligned row chunk, fewest nonzeros first: colind/vals "
-                       "H2D -> device colind check -> kernel -> C rows D2H overlapping the next "
-                       "chunk; wall clock per call)"}
+        e2e = m.e2e_single(flops, reps) if world == 1 else m.e2e_sharded(flops, args.b_panels, reps)
 
-    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_port(csr, B, N)
+        if getattr(m, "host", None) is not None:
+            h_rp, h_ci, h_v, h_B = (t.numpy() for t in m.host)
+        else:
+            h_rp, h_ci, h_v, h_B = (t.cpu().numpy() for t in (m.rowptr, m.colind, m.vals, m.B))
+        cpu = cpu_baseline_port(h_rp, h_ci, h_v, h_B, N, args.op)
 
+    info = m.info
+    line = None
     if rank == 0:
         line = {
             "metric": "SpMM GFLOP/s (2*nnz*N)",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_job, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+            "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic" + (f" ({world} row-stacked copies of the workload sharing B, one per rank)"
                                    if world > 1 and args.scaling == "weak" else ""),
-            "config": {"workload": spec["desc"], "op": args.op, "N": N, "M": M_all, "K": K,
-                       "nnz": nnz_all, "l2_flush": f"{flush.numel() * 4 >> 20} MiB written between timed steps",
+            "config": {"workload": m.spec["desc"], "op": args.op, "N": N, "M": m.M_all, "K": K,
+                       "nnz": m.nnz_all, "input": m.fp,
+                       "generator": ("torch ops (workloads.rmat_csr), same seed as the reference arm"
+                                     if args.generator == "torch" else "libgespmm gespmm_rmat_csr"),
+                       "l2_flush": f"{m.flush.numel() * 4 >> 20} MiB written between timed steps",
                        "parallelism": (f"row-block x{world} ({args.scaling} scaling)" if world > 1
                                        else "single GPU"),
                        "plan": {"n_items": info["n_items"], "n_long_rows": info["n_long_rows"],
-                                "n_segments": info["n_segments"], "build_ms": plan_ms,
-                                "build_wall_ms": plan_wall_ms},
-                       "b_broadcast_ms": bcast_ms},
-            "hbm_gbs_algorithmic": achieved,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "bytes_model": f"U = 4(M+1) + 8nnz + 4KN + 4MN = {U} B per launch",
-                         "peak_source": peak_src,
-                         "gather_bytes_G": G, "gather_GBs": G / (t_mean * 1e-3) / 1e9,
-                         "gather_ceiling": gather_ceiling, "ncu": ncu},
+                                "n_segments": info["n_segments"], "build_ms": m.plan_ms,
+                                "build_wall_ms": m.plan_wall_ms},
+                       "b_broadcast_ms": m.bcast_ms},
+            "hbm_gbs_algorithmic": roof["achieved"],
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
             "sustained": sustained,
+            "broadcast": broadcast,
             "c_allgather": c_allgather,
             "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]) * n_panels,
             "panel_cols": pw,
-            "kernel_variant": variant_name(N, B, C, args.op),
+            "kernel_variant": variant_name(N, m.B, m.C, args.op),
             "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
         }
+    del m
+    torch.cuda.empty_cache()
+    extras = [w for w in args.extra.split(",") if w and w != args.workload] if world == 1 else []
+    if extras and rank == 0:
+        line["extra"] = {}
+        for w in extras:
+            try:
+                line["extra"][w] = measure_extra(args, w, dev)
+            except Exception as ex:  # report, never fail the headline line
+                line["extra"][w] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

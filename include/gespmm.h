@@ -308,6 +308,47 @@ gespmm_status_t gespmm_sharded_spmm_chunked(void* comm, int world, int rank, int
                                             int accumulate, float* C_full, int64_t ldc_full,
                                             const int64_t* row_bounds, int chunks, void* stream);
 
+/* Options of gespmm_sharded_spmm_ex. */
+typedef struct {
+  /* > 1: B is broadcast in this many column panels (widths multiples of 32
+   * where N allows), panel p on an internal comm stream while panel p-1
+   * computes; non-root ranks' B is then NOT written --
+   * the panels live in b_panel_ws.  1: one in-place broadcast of B. */
+  int b_panels;
+  /* K*N floats of device workspace for the panels; NULL: allocated and freed
+   * stream-ordered per call. */
+  float* b_panel_ws;
+  /* > 1: C all-gather overlapped with the compute in this many row chunks
+   * (needs b_panels == 1). */
+  int c_chunks;
+  /* > 0: return only after the work drained, polling ncclCommGetAsyncError;
+   * an asynchronous NCCL error or a wait longer than timeout_ms ABORTS the
+   * communicator (ncclCommAbort) and returns GESPMM_NCCL_ERROR -- a dead peer
+   * is an error, not a hang.  0: asynchronous on `stream` (the internal
+   * waits use GESPMM_NCCL_TIMEOUT_MS, default 600000). */
+  int64_t timeout_ms;
+} gespmm_shard_opts_t;
+
+/* Row-sharded SpMM with options (the two entry points above are this with
+ * {1, NULL, 1, 0} and {1, NULL, chunks, 0}).  With plan == NULL a temporary
+ * plan VALIDATES this rank's CSR (colind range included) before any
+ * collective, and the ranks agree on the outcome with one all-reduce: a rank
+ * whose block is invalid returns GESPMM_CSR_INVALID and every other rank
+ * returns it too (no rank is left waiting in a broadcast). */
+gespmm_status_t gespmm_sharded_spmm_ex(void* comm, int world, int rank, int root, gespmm_plan_t plan,
+                                       int64_t M_local, int64_t K, int64_t N, int64_t nnz_local,
+                                       const int32_t* rowptr, const int32_t* colind, const float* vals,
+                                       float* B, int64_t ldb, float* C, int64_t ldc, gespmm_reduce_t op,
+                                       int accumulate, float* C_full, int64_t ldc_full,
+                                       const int64_t* row_bounds, const gespmm_shard_opts_t* opts,
+                                       void* stream);
+
+/* Waits for `stream` while polling ncclCommGetAsyncError(comm): GESPMM_OK when
+ * the stream drained; on an asynchronous NCCL error or after timeout_ms (> 0)
+ * the communicator is aborted (ncclCommAbort; a later gespmm_comm_destroy is a
+ * no-op) and GESPMM_NCCL_ERROR is returned. */
+gespmm_status_t gespmm_comm_wait(void* comm, void* stream, int64_t timeout_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,11 @@ EXTRA = os.environ.get("GESPMM_EXTRA_FLAGS", "").split()
 if TAG:
     LIB = os.path.join(PKG, f"libgespmm_{TAG}.so")
     BUILD = os.path.join(PKG, f"build_{TAG}")
+    # experiment knobs (incl. the wrong-result GESPMM_ABL_* ablations) compile
+    # only into tagged libraries, never into the product libgespmm.so
+    EXTRA = EXTRA + ["-DGESPMM_EXPERIMENT_BUILD"]
+elif EXTRA:
+    raise SystemExit("GESPMM_EXTRA_FLAGS needs GESPMM_BUILD_TAG (experiment builds go to libgespmm_<tag>.so)")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -28,12 +28,18 @@ EXPORTS = [
     "gespmm_panel_width", "gespmm_set_schedule_override", "gespmm_set_tile_work_override", "gespmm_partition_rows",
     "gespmm_rmat_csr", "gespmm_uniform_fill", "gespmm_coo_to_csr", "gespmm_csr_transpose",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
-    "gespmm_sharded_spmm_chunked",
+    "gespmm_sharded_spmm_chunked", "gespmm_sharded_spmm_ex", "gespmm_comm_wait",
 ]
 
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
 _vp = ctypes.c_void_p
+
+
+class ShardOpts(ctypes.Structure):
+    """gespmm_shard_opts_t"""
+    _fields_ = [("b_panels", ctypes.c_int), ("b_panel_ws", ctypes.c_void_p), ("c_chunks", ctypes.c_int),
+                ("timeout_ms", ctypes.c_int64)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -98,6 +104,10 @@ def load():
         "gespmm_sharded_spmm_chunked": ([_vp, _int, _int, _int, _vp, _i64, _i64, _i64, _i64, _vp, _vp,
                                          _vp, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64, _vp, _int,
                                          _vp], _int),
+        "gespmm_sharded_spmm_ex": ([_vp, _int, _int, _int, _vp, _i64, _i64, _i64, _i64, _vp, _vp,
+                                    _vp, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64, _vp,
+                                    ctypes.POINTER(ShardOpts), _vp], _int),
+        "gespmm_comm_wait": ([_vp, _vp, _i64], _int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -281,6 +281,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #ifndef GESPMM_ABL_NOGATHER
 #define GESPMM_ABL_NOGATHER 0
 #endif
+// the ablations skip the gathers / the C stores (wrong results by design): only
+// tagged experiment builds (_build.py: GESPMM_BUILD_TAG -> libgespmm_<tag>.so,
+// -DGESPMM_EXPERIMENT_BUILD) may set them, never the product library
+#if (GESPMM_ABL_NOSTORE || GESPMM_ABL_NOGATHER) && !defined(GESPMM_EXPERIMENT_BUILD)
+#error "GESPMM_ABL_NOSTORE/NOGATHER give wrong results: tagged experiment builds only (GESPMM_BUILD_TAG)"
+#endif
 template <int CPL>
 struct Pipe {
   static constexpr int U = CPL >= 4 ? 4 : GESPMM_U_NARROW;

@@ -113,6 +113,9 @@ struct Semiring<GESPMM_REDUCE_MEAN> {
   }
   __device__ __forceinline__ static float finalize(float acc, int deg, bool accumulate, float c0) {
 #ifdef GESPMM_ABL_MEANMUL  // ablation builds only: the division's cost
+#ifndef GESPMM_EXPERIMENT_BUILD
+#error "GESPMM_ABL_MEANMUL gives wrong results: tagged experiment builds only (GESPMM_BUILD_TAG)"
+#endif
     float r = deg ? acc * static_cast<float>(deg) : 0.0f;
 #else
     float r = deg ? __fdiv_rn(acc, static_cast<float>(deg)) : 0.0f;

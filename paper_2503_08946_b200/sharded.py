@@ -46,6 +46,69 @@ def broadcast_B(B, root: int = 0, group=None):
     return B
 
 
+def panel_bounds(N: int, panels: int):
+    """Column panels [c0, c1) of B for the overlapped broadcast: `panels`
+    near-equal widths, multiples of 32 columns where N allows (one warp row
+    per panel row), never empty."""
+    panels = max(1, min(int(panels), max(1, N // 32) if N >= 32 else 1))
+    step = -(-N // panels)
+    if N >= 32:
+        step = -(-step // 32) * 32
+    out, c0 = [], 0
+    while c0 < N:
+        out.append((c0, min(N, c0 + step)))
+        c0 += step
+    return out
+
+
+def broadcast_B_overlapped(compute_panel, B, panels: int, root: int = 0, group=None, cuda_streams=None,
+                           packed=None):
+    """The B broadcast overlapped with the compute.
+
+    B (K x N, row-major) is cut into column panels; the root packs panel p
+    into a contiguous K x w buffer (NCCL moves contiguous bytes), panel p is
+    broadcast on the comm stream while panel p-1 computes, and
+    ``compute_panel(p, Bp, c0, c1)`` runs on the compute stream as soon as
+    panel p has landed (C[:, c0:c1] from the K x w panel, ldb = w).  Time is
+    max(broadcast, compute) + one panel of the other, instead of their sum.
+    Each column's reduction does not depend on which other columns share its
+    launch, so results are bit-identical to the unpanelled path (tested).
+
+    ``packed``: optional list of preallocated K x w panel buffers (reused
+    across calls).  Non-root ranks' B is not written (the panels hold the
+    broadcast data).  ``cuda_streams`` = (compute, comm) torch streams on
+    GPUs; None runs the same schedule synchronously (gloo/CPU).  Returns the
+    list of panel buffers."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    K, N = B.shape
+    pb = panel_bounds(N, panels)
+    if packed is None:
+        packed = [torch.empty((K, c1 - c0), dtype=B.dtype, device=B.device) for c0, c1 in pb]
+    if cuda_streams is None:
+        for p, (c0, c1) in enumerate(pb):
+            if rank == root:
+                packed[p].copy_(B[:, c0:c1])
+            dist.broadcast(packed[p], src=root, group=group)
+            compute_panel(p, packed[p], c0, c1)
+        return packed
+    comp, comm = cuda_streams
+    comm.wait_stream(comp)  # B and the panel buffers are ready on the compute stream
+    for p, (c0, c1) in enumerate(pb):
+        with torch.cuda.stream(comm):
+            if rank == root:
+                packed[p].copy_(B[:, c0:c1])
+            dist.broadcast(packed[p], src=root, group=group)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+        comp.wait_event(ev)
+        with torch.cuda.stream(comp):
+            compute_panel(p, packed[p], c0, c1)
+    return packed
+
+
 def gather_C(C_local, bounds, group=None):
     """All ranks receive the full C (rows bounds[-1] x N) -- one broadcast per
     slab owner, since slabs are uneven."""
@@ -143,12 +206,18 @@ class ShardedSpMM:
             self._plan = Plan(rowptr_local, colind_local, K)
 
     def __call__(self, vals_local, B, reduce: str = "sum", gather=False,
-                 broadcast: bool = True, chunks: int = 1):
+                 broadcast: bool = True, chunks: int = 1, b_panels: int = 1):
         """gather=True: C all-gather after the compute (one broadcast per slab
         owner), overlapped with it when chunks > 1 (gather_C_overlapped);
         gather="peer": FUSED into the kernel -- every C row is stored straight
         into every rank's full-C buffer over NVLink (CUDA IPC), no collective
-        (gespmm_plan_execute_peers)."""
+        (gespmm_plan_execute_peers).
+        b_panels > 1 (with broadcast): the B broadcast is cut into column
+        panels overlapped with the compute (broadcast_B_overlapped); the
+        result is this rank's C slab (gathered afterwards if asked)."""
+        if broadcast and b_panels > 1 and gather != "peer":
+            C = self._compute_panelled(vals_local, B, reduce, b_panels)
+            return gather_C(C, self.bounds, self.group) if gather else C
         if broadcast:
             broadcast_B(B, self.root, self.group)
         if gather == "peer":
@@ -161,6 +230,33 @@ class ShardedSpMM:
             C = self._plan.execute(vals_local, B, reduce)
         if gather:
             return gather_C(C, self.bounds, self.group)
+        return C
+
+    def _compute_panelled(self, vals_local, B, reduce, panels):
+        import torch
+
+        M = self.rowptr.shape[0] - 1
+        N = B.shape[1]
+        if self._compute is not None:  # injected (CPU tests): one call per panel
+            C = torch.empty((M, N), dtype=torch.float32, device=B.device)
+
+            def panel(p, Bp, c0, c1):
+                C[:, c0:c1] = self._compute(self.rowptr, self.colind, vals_local, Bp, reduce)
+            broadcast_B_overlapped(panel, B, panels, self.root, self.group)
+            return C
+        C = torch.empty((M, N), dtype=torch.float32, device=B.device)
+        comp = torch.cuda.current_stream(B.device)
+        if self._comm_stream is None:
+            self._comm_stream = torch.cuda.Stream(device=B.device)
+
+        def panel(p, Bp, c0, c1):
+            self._plan.execute(vals_local, Bp, reduce, out=C[:, c0:c1], stream=comp)
+        packed = getattr(self, "_packed", None)
+        want = [(B.shape[0], c1 - c0) for c0, c1 in panel_bounds(N, panels)]
+        if packed is None or [tuple(t.shape) for t in packed] != want or packed[0].device != B.device:
+            packed = None
+        self._packed = broadcast_B_overlapped(panel, B, panels, self.root, self.group,
+                                              cuda_streams=(comp, self._comm_stream), packed=packed)
         return C
 
     def _gather_overlapped(self, vals_local, B, reduce, chunks):

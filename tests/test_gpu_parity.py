@@ -795,6 +795,121 @@ def test_capi_sharded_spmm_single_rank(cuda, oracle_mod, chunks):
         L.gespmm_comm_destroy(comm)
 
 
+@pytest.mark.parametrize("panels,gather", [(2, False), (3, True), (4, True)])
+def test_capi_sharded_spmm_ex_panelled_broadcast(cuda, oracle_mod, panels, gather):
+    """gespmm_sharded_spmm_ex with the B broadcast in column panels overlapped
+    with the compute (world 1 over NCCL on the one GPU), with and
+    without a caller workspace, bounded error-polled wait: bit-exact to the
+    twin for N = 128 (4 x 32 panels) and a ragged N = 80."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_08946_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(61)
+    M, K = 9_000, 1_500
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 10, [(100, 900)])
+    uid = ctypes.create_string_buffer(128)
+    _lib.check(L.gespmm_comm_get_unique_id(uid))
+    comm = ctypes.c_void_p()
+    _lib.check(L.gespmm_comm_init(ctypes.byref(comm), 1, uid, 0))
+    try:
+        for N, op in ((128, "sum"), (80, "max")):
+            B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+            rp, ci, vv, Bt = to_dev(cuda, rowptr, colind, vals, B)
+            C = torch.full((M, N), float("nan"), device=cuda)
+            Cf = torch.full((M, N), float("nan"), device=cuda) if gather else None
+            ws = torch.empty(K * N, device=cuda) if panels == 3 else None
+            bounds = (ctypes.c_int64 * 2)(0, M)
+            o = _lib.ShardOpts(panels, ws.data_ptr() if ws is not None else None, 1, 60_000)
+            s = torch.cuda.current_stream(cuda).cuda_stream
+            _lib.check(L.gespmm_sharded_spmm_ex(
+                comm, 1, 0, 0, None, M, K, N, int(rowptr[-1]), rp.data_ptr(), ci.data_ptr(), vv.data_ptr(),
+                Bt.data_ptr(), N, C.data_ptr(), N, {"sum": 0, "max": 1}[op], 0,
+                Cf.data_ptr() if gather else None, N, bounds, ctypes.byref(o), s))
+            torch.cuda.synchronize()
+            want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG)
+            np.testing.assert_array_equal(C.cpu().numpy(), want)
+            if gather:
+                np.testing.assert_array_equal(Cf.cpu().numpy(), want)
+    finally:
+        L.gespmm_comm_destroy(comm)
+
+
+def test_capi_sharded_spmm_ex_validates_before_any_collective(cuda):
+    """No plan passed: the temporary plan validates colind before the B
+    broadcast: an out-of-range column is GESPMM_CSR_INVALID, not an
+    out-of-bounds gather; the communicator stays usable."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_08946_b200 import _lib
+    from paper_2503_08946_b200.errors import Error, ErrorKind
+
+    L = _lib.load()
+    rng = np.random.default_rng(62)
+    M, K, N = 500, 300, 64
+    rowptr, colind, vals = random_csr(rng, M, K, 0.05)
+    bad = colind.copy()
+    bad[len(bad) // 2] = K + 5
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    uid = ctypes.create_string_buffer(128)
+    _lib.check(L.gespmm_comm_get_unique_id(uid))
+    comm = ctypes.c_void_p()
+    _lib.check(L.gespmm_comm_init(ctypes.byref(comm), 1, uid, 0))
+    try:
+        s = torch.cuda.current_stream(cuda).cuda_stream
+        C = torch.empty((M, N), device=cuda)
+        for panels in (1, 2):
+            rp, ci, vv, Bt = to_dev(cuda, rowptr, bad, vals, B)
+            o = _lib.ShardOpts(panels, None, 1, 60_000)
+            with pytest.raises(Error) as ei:
+                _lib.check(L.gespmm_sharded_spmm_ex(
+                    comm, 1, 0, 0, None, M, K, N, int(rowptr[-1]), rp.data_ptr(), ci.data_ptr(), vv.data_ptr(),
+                    Bt.data_ptr(), N, C.data_ptr(), N, 0, 0, None, N, None, ctypes.byref(o), s))
+            assert ei.value.kind == ErrorKind.CsrInvalid
+        torch.cuda.synchronize()
+        ci = torch.as_tensor(colind, device=cuda)
+        _lib.check(L.gespmm_sharded_spmm_ex(
+            comm, 1, 0, 0, None, M, K, N, int(rowptr[-1]), rp.data_ptr(), ci.data_ptr(), vv.data_ptr(),
+            Bt.data_ptr(), N, C.data_ptr(), N, 0, 0, None, N, None, ctypes.byref(o), s))
+        torch.cuda.synchronize()
+    finally:
+        L.gespmm_comm_destroy(comm)
+
+
+def test_comm_wait_timeout_aborts_instead_of_hanging(cuda):
+    """gespmm_comm_wait polls ncclCommGetAsyncError while the stream runs; a
+    wait past its bound (here: a stream held by a ~1 s spin kernel, standing in
+    for a collective whose peer died) aborts the communicator and returns
+    GESPMM_NCCL_ERROR; destroying the aborted comm is a no-op; a short wait on
+    an idle stream is OK."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_08946_b200 import _lib
+
+    L = _lib.load()
+    uid = ctypes.create_string_buffer(128)
+    _lib.check(L.gespmm_comm_get_unique_id(uid))
+    comm = ctypes.c_void_p()
+    _lib.check(L.gespmm_comm_init(ctypes.byref(comm), 1, uid, 0))
+    stream = torch.cuda.Stream(device=cuda)
+    assert L.gespmm_comm_wait(comm, stream.cuda_stream, 1000) == 0
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(2_000_000_000)  # ~1 s of GPU clock cycles
+    rc = L.gespmm_comm_wait(comm, stream.cuda_stream, 50)
+    assert rc == 5, rc  # GESPMM_NCCL_ERROR
+    assert b"timed out" in L.gespmm_last_error()
+    stream.synchronize()
+    assert L.gespmm_comm_wait(comm, stream.cuda_stream, 50) == 5  # aborted: stays an error
+    assert L.gespmm_comm_destroy(comm) == 0
+
+
 @pytest.mark.parametrize("op", OPS)
 def test_64bit_b_offsets(cuda, oracle_mod, op):
     """K * ldb > 2^32: the kernel's 64-bit B-row addressing path (staged 32-bit

@@ -1,5 +1,6 @@
 """Multi-rank host logic of the row-sharded path on CPU (gloo, world size 2 and
-4): partition, B broadcast from the root (the only exchange), per-rank slabs,
+4): partition, B broadcast from the root (the only exchange; whole, or in
+column panels overlapped with the compute), per-rank slabs,
 uneven C all-gather -- and the result is bit-identical to the single-process
 computation (the per-rank compute here is the oracle's fp32 twin, the same
 semantics the GPU path is bit-exact to)."""
@@ -66,6 +67,13 @@ def _worker(rank, world, port, q):
             Cc = shc(vv, B, op, gather=True, chunks=3, broadcast=False)  # overlapped all-gather
             assert np.array_equal(Cc.numpy(), out[op]), op
         assert np.array_equal(B.numpy(), B_full)  # broadcast reached every rank
+        # B broadcast in column panels overlapped with the compute (f4): B96 is
+        # only on the root; 3 panels of 32 columns, bit-identical to one launch
+        B96_full = np.random.default_rng(11).uniform(-1, 1, (B_full.shape[0], 96)).astype(np.float32)
+        for op in ("sum", "max"):
+            B96 = torch.from_numpy(B96_full.copy()) if rank == 0 else torch.zeros(B96_full.shape)
+            Cp = sh(vv, B96, op, gather=True, b_panels=3)
+            out[op + "96"] = Cp.numpy()
         q.put((rank, out, bounds.tolist()))
     finally:
         dist.destroy_process_group()
@@ -90,5 +98,10 @@ def test_sharded_gloo_bit_identical(world, oracle_mod):
         want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=256)
         for rank, out, bounds in results:
             np.testing.assert_array_equal(out[op], want)
+        if op in ("sum", "max"):
+            B96 = np.random.default_rng(11).uniform(-1, 1, (B.shape[0], 96)).astype(np.float32)
+            want96 = oracle_mod.spmm_f32(rowptr, colind, vals, B96, op, seg_len=256)
+            for rank, out, bounds in results:
+                np.testing.assert_array_equal(out[op + "96"], want96)
     b = results[0][2]
     assert b[0] == 0 and b[-1] == len(rowptr) - 1 and all(x <= y for x, y in zip(b, b[1:]))
