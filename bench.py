@@ -929,13 +929,14 @@ def main():
         }
     del m
     torch.cuda.empty_cache()
-    extras = [w for w in args.extra.split(",") if w and w != args.workload] if world == 1 else []
+    extras = [w.strip("'\" ") for w in args.extra.split(",")] if world == 1 else []
+    extras = [w for w in extras if w and w != "none" and w != args.workload]
     if extras and rank == 0:
         line["extra"] = {}
         for w in extras:
             try:
                 line["extra"][w] = measure_extra(args, w, dev)
-            except Exception as ex:  # report, never fail the headline line
+            except (Exception, SystemExit) as ex:  # report, never fail the headline line
                 line["extra"][w] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     if rank == 0:
         print(json.dumps(line))

@@ -125,6 +125,12 @@ Variant pick_variant(int64_t N, const float* B, int64_t ldb, const float* C, int
   return v;
 }
 
+// Plan-owned device buffers (items, partials, counters, work counters, the
+// hot set) come from the device's stream-ordered pool (cudaMallocAsync on the
+// plan's stream; the pool keeps its memory mapped, gespmm_plan.cu
+// keep_pool_resident), so a fresh plan costs no cudaMalloc round trip
+// (config 2: 1.46 ms per fresh Plan with cudaMalloc); grow-only, released with
+// cudaFree (synchronizing) in gespmm_plan_destroy.
 gespmm_status_t ensure_workspace(gespmm_plan_s* plan, int64_t ldp, int ncb, cudaStream_t s) {
   if (plan->n_segs == 0) return GESPMM_OK;
   const int64_t need_p = plan->n_segs * ldp;
@@ -132,7 +138,7 @@ gespmm_status_t ensure_workspace(gespmm_plan_s* plan, int64_t ldp, int ncb, cuda
     if (plan->partials) cudaFree(plan->partials);
     plan->partials = nullptr;
     plan->partial_floats = 0;
-    cudaError_t e = cudaMalloc(&plan->partials, static_cast<size_t>(need_p) * sizeof(float));
+    cudaError_t e = cudaMallocAsync(&plan->partials, static_cast<size_t>(need_p) * sizeof(float), s);
     if (e != cudaSuccess) return cuda_fail(e, "plan partials");
     plan->partial_floats = need_p;
   }
@@ -141,7 +147,7 @@ gespmm_status_t ensure_workspace(gespmm_plan_s* plan, int64_t ldp, int ncb, cuda
     if (plan->counters) cudaFree(plan->counters);
     plan->counters = nullptr;
     plan->counter_ints = 0;
-    cudaError_t e = cudaMalloc(&plan->counters, static_cast<size_t>(need_c) * sizeof(int));
+    cudaError_t e = cudaMallocAsync(&plan->counters, static_cast<size_t>(need_c) * sizeof(int), s);
     if (e != cudaSuccess) return cuda_fail(e, "plan counters");
     e = cudaMemsetAsync(plan->counters, 0, static_cast<size_t>(need_c) * sizeof(int), s);
     if (e != cudaSuccess) return cuda_fail(e, "plan counters memset");
@@ -238,6 +244,45 @@ int64_t panel_width(int64_t K, int64_t N) {
   return w < N ? w : N;
 }
 
+// L2 hot-set size in B rows for one launch (0: off).  On when the gathered B
+// slab (K x n fp32) is at least GESPMM_HOT_MIN_X (4) times the L2 size, the
+// tile is the 128-column register tile (512-byte rows) and 32-bit offsets
+// leave bit 31 free (K*ldb <= 2^31); H = GESPMM_HOT_MB (64 MB) of rows.
+// GESPMM_HOT=0 disables it.  Measured on config 5's column stream
+// (tools/l2hot_probe.cu, profiles/r2_l2hot_probe_config5.jsonl): 64 MB of hot
+// rows evict_last + cold rows evict_first 44.1 -> 39.1 ms (register gathers,
+// 4 rows in flight per warp); a persisting access-policy window on a compact
+// copy of the hot rows, or the hot rows alone evict_last, gained less.
+int g_hot_override = -1;  // gespmm_set_hot_override: -1 auto, 0 off, 1 any size
+int64_t hot_rows(int64_t K, int64_t n, int64_t ldb, const Variant& v) {
+  static const int env_mode = [] {  // measured slower than the ring: off by default
+    const char* e = std::getenv("GESPMM_HOT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int mode = g_hot_override == 0 ? 0 : g_hot_override == 1 ? 2 : env_mode;
+  static const int64_t mb = [] {
+    const char* e = std::getenv("GESPMM_HOT_MB");
+    const long long x = e ? std::atoll(e) : 64;
+    return static_cast<int64_t>(x > 0 ? x : 64);
+  }();
+  static const int64_t min_x = [] {
+    const char* e = std::getenv("GESPMM_HOT_MIN_X");
+    const long long x = e ? std::atoll(e) : 4;
+    return static_cast<int64_t>(x > 0 ? x : 4);
+  }();
+  if (mode == 0 || v.pair || v.vec != 4 || v.cwm != 1 || n <= 0) return 0;
+  if (K * ldb > (int64_t(1) << 31)) return 0;
+  static int64_t l2 = [] {
+    int dev = 0, b = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&b, cudaDevAttrL2CacheSize, dev);
+    return static_cast<int64_t>(b > 0 ? b : (126 << 20));
+  }();
+  if (mode != 2 && K * n * 4 < min_x * l2) return 0;  // GESPMM_HOT=2: any size (tests)
+  const int64_t H = (mb << 20) / (n * 4);
+  return H < 1 ? 1 : H;
+}
+
 // The launches of one execute (one per column panel), optionally restricted
 // to the item range *range (device memory) with an on-device abort flag.
 gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* rowptr,
@@ -245,6 +290,7 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
                               float* C, int64_t ldc, gespmm_reduce_t op, int accumulate,
                               const int64_t* range, const int* abort_flag, cudaStream_t s,
                               float* const* peers = nullptr, int n_peers = 0, int64_t peer_shift = 0) {
+  NvtxRange nvtx(n_peers > 0 ? "gespmm:execute_peers" : range ? "gespmm:execute_range" : "gespmm:execute");
   gespmm_status_t st = GESPMM_OK;
   // Column panels (DESIGN.md 5.2 "Panels"): when B's row slab K x N does not
   // fit in L2, the columns are processed in panels of `pw` columns, one launch
@@ -287,6 +333,11 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     p.off32 = plan->K * ldb <= (int64_t(1) << 32);
     p.range = range;
     p.abort_flag = abort_flag;
+    p.n_items_dev = nullptr;
+    if (plan->async_counts) {  // build_plan_async: true count + error bits on the device
+      p.n_items_dev = &plan->meta->n_items;
+      if (!p.abort_flag) p.abort_flag = &plan->meta->err;
+    }
     // Dynamic item distribution for launches with enough items to balance
     // (config 1's 1.3 K items ran 0.018 -> 0.029 ms dynamic: the counter reset
     // dominates); the counters (one per column block) are zeroed on the
@@ -301,7 +352,7 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
         if (plan->work_ctr) cudaFree(plan->work_ctr);
         plan->work_ctr = nullptr;
         plan->work_ctr_n = 0;
-        cudaError_t e = cudaMalloc(&plan->work_ctr, static_cast<size_t>(ncb) * 8);
+        cudaError_t e = cudaMallocAsync(&plan->work_ctr, static_cast<size_t>(ncb) * 8, s);
         if (e != cudaSuccess) return cuda_fail(e, "plan work counters");
         plan->work_ctr_n = ncb;
       }
@@ -312,6 +363,19 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     p.n_peers = n_peers;
     p.peer_shift = peer_shift;
     for (int q = 0; q < n_peers; ++q) p.peers[q] = peers[q] + c0;  // this panel's columns
+    // L2 hot set (gespmm_hot.cu): B many times larger than L2, 512-byte rows
+    // (the 128-column register tile), whole-plan launches only; built once
+    // per plan and size, on the stream (no host sync)
+    p.hot_bits = nullptr;
+    p.hot_K = static_cast<int>(plan->K);
+    const int64_t H = hot_rows(plan->K, n, ldb, v);
+    if (H > 0 && !range && !abort_flag && n_peers == 0 && plan->nnz > 0) {
+      if (plan->hot_key != H) {
+        cudaError_t he = build_hot_bits(plan, colind, H, s);
+        if (he != cudaSuccess) return cuda_fail(he, "L2 hot set");
+      }
+      p.hot_bits = plan->hot_bits;
+    }
     cudaError_t e = launch_spmm(op, v, p, s);
     if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
   }
@@ -444,7 +508,7 @@ gespmm_status_t gespmm_plan_execute_rows(gespmm_plan_t plan, int64_t row_begin, 
   DeviceGuard dg(plan->device);
   cudaStream_t s = as_stream(stream);
   if (!plan->row_range) {
-    cudaError_t e = cudaMalloc(&plan->row_range, 4 * sizeof(int64_t));
+    cudaError_t e = cudaMallocAsync(&plan->row_range, 4 * sizeof(int64_t), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(plan->row_range, 0, 4 * sizeof(int64_t), s);
     if (e != cudaSuccess) return cuda_fail(e, "plan row range");
   }
@@ -524,6 +588,9 @@ gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
   if (plan->items) cudaFree(plan->items);
   if (plan->partials) cudaFree(plan->partials);
   if (plan->counters) cudaFree(plan->counters);
+  if (plan->hot_bits) cudaFree(plan->hot_bits);
+  if (plan->meta) cudaFree(plan->meta);
+  if (plan->meta_host) cudaFreeHost(plan->meta_host);
   delete plan;
   return GESPMM_OK;
 }
@@ -546,6 +613,7 @@ gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
                                 const int32_t* rowptr, const int32_t* colind,
                                 const float* vals, const float* B, int64_t ldb, float* C,
                                 int64_t ldc, gespmm_reduce_t op, int accumulate, void* stream) {
+  NvtxRange nvtx("gespmm:csr_spmm");
   g_last_error.clear();
   gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
   if (st != GESPMM_OK) return st;
@@ -569,12 +637,26 @@ gespmm_status_t gespmm_csr_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz,
   plan->M = M;
   plan->K = K;
   plan->nnz = nnz;
-  st = build_plan(plan, rowptr, colind, /*validate colind*/ true, as_stream(stream));
+  // one synchronization per call: the plan is built on the device without a
+  // host round trip (build_plan_async), the kernel reads its item count and
+  // error bits there, and the bits come back with the trailing sync
+  cudaStream_t cs = as_stream(stream);
+  st = build_plan_async(plan, rowptr, colind, /*validate colind*/ true, cs);
   if (st != GESPMM_OK) return st;
   st = gespmm_plan_execute(plan, N, rowptr, colind, vals, B, ldb, C, ldc, op, accumulate, stream);
-  const cudaError_t e = cudaStreamSynchronize(as_stream(stream));
-  if (st == GESPMM_OK && e != cudaSuccess) return cuda_fail(e, "spmm");
-  return st;
+  if (st != GESPMM_OK) {
+    cudaStreamSynchronize(cs);
+    return st;
+  }
+  cudaError_t e = plan->n_items > 0 ? cudaMemcpyAsync(plan->meta_host, plan->meta, sizeof(*plan->meta),
+                                                     cudaMemcpyDeviceToHost, cs)
+                                   : cudaSuccess;
+  const cudaError_t e2 = cudaStreamSynchronize(cs);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(e, "spmm");
+  if (plan->n_items > 0 && plan->meta_host->err)
+    return fail(GESPMM_CSR_INVALID, csr_error_message(plan->meta_host->err, K));
+  return GESPMM_OK;
 }
 
 gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
@@ -582,6 +664,7 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
                                      const float* vals, const float* B, int64_t ldb, float* C,
                                      int64_t ldc, gespmm_reduce_t op, int accumulate,
                                      void* stream) {
+  NvtxRange nvtx("gespmm:csr_spmm_host");
   g_last_error.clear();
   gespmm_status_t st = check_shape(M, K, N, nnz, ldb, ldc);
   if (st != GESPMM_OK) return st;
@@ -786,6 +869,12 @@ int64_t gespmm_panel_width(int64_t K, int64_t N) { return N < 1 ? 0 : panel_widt
 gespmm_status_t gespmm_set_schedule_override(int mode) {
   if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: schedule mode -1/0/1");
   g_schedule_override = mode;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_set_hot_override(int mode) {
+  if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: hot mode -1/0/1");
+  g_hot_override = mode;
   return GESPMM_OK;
 }
 

@@ -149,6 +149,7 @@ gespmm_status_t gespmm_comm_destroy(void* comm) {
 }
 
 gespmm_status_t gespmm_comm_wait(void* comm, void* stream, int64_t timeout_ms) {
+  gespmm::NvtxRange nvtx("gespmm:comm_wait");
   Nccl& n = nccl();
   if (!n.ok) return gespmm::fail(GESPMM_NOT_SUPPORTED, n.why);
   if (!comm) return gespmm::fail(GESPMM_INVALID_ARG, "invalid argument: comm is null");
@@ -178,6 +179,7 @@ gespmm_status_t gespmm_sharded_spmm_ex(void* comm, int world, int rank, int root
                                        int accumulate, float* C_full, int64_t ldc_full,
                                        const int64_t* row_bounds, const gespmm_shard_opts_t* opts,
                                        void* stream) {
+  gespmm::NvtxRange nvtx("gespmm:sharded_spmm");
   Nccl& n = nccl();
   if (!n.ok) return gespmm::fail(GESPMM_NOT_SUPPORTED, n.why);
   gespmm_shard_opts_t o = {1, nullptr, 1, 0};

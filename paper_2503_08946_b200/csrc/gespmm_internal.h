@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -103,6 +104,9 @@ struct KParams {
   // check of this or an earlier chunk, with or without a range).
   const int64_t* range;
   const int* abort_flag;
+  // one-shot plans built without a host sync (build_plan_async): the true
+  // item count lives on the device (n_items above is its upper bound)
+  const int64_t* n_items_dev;
   // Fused C all-gather (gespmm_plan_execute_peers): every C row is also stored
   // at peers[q] + peer_shift + (its offset from C), q < n_peers -- peer GPUs'
   // full-C buffers (CUDA IPC over NVLink) or this GPU's own.
@@ -111,6 +115,10 @@ struct KParams {
   int64_t peer_shift;
   // dynamic item distribution: one counter per column block, zero at launch
   unsigned long long* work_ctr;
+  // L2 hot set (gespmm_hot.cu; nullptr: off): bit c set = column c's B row
+  // is gathered with L2 evict_last, every other row with evict_first
+  const uint32_t* hot_bits;
+  int hot_K;
 };
 
 // GESPMM_TRACE=1: phase timings of the host entry point and the plan build on
@@ -121,6 +129,16 @@ struct Trace {
   const char* scope = "";
   explicit Trace(const char* s);
   void mark(const char* phase, cudaStream_t stream);
+};
+
+// NVTX range for the host-side phases (plan build, execute, the pipelined
+// host entry point, the sharded path): visible in nsys / ncu --nvtx timelines.
+// Header-only NVTX v3: a no-op unless a profiler injects its library.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 void set_error(const std::string& msg);
@@ -153,4 +171,27 @@ struct gespmm_plan_s {
   int64_t counter_ints = 0;
   int tile_work = gespmm::kTileWork;
   int device = 0;
+  // L2 hot set of B rows (gespmm_hot.cu), built at the first execute that
+  // wants one; hot_key = its size H in rows (-1: none / stale after re-plan)
+  uint32_t* hot_bits = nullptr;
+  int64_t hot_words = 0;
+  int64_t hot_key = -1;
+  // build_plan_async (the one-shot entry point): counts and the CSR error
+  // bits stay on the device (meta); n_items / n_segs hold upper bounds and
+  // every launch reads the true count and aborts on an error bit
+  struct Meta {
+    int64_t n_items, n_segs;
+    int err, n_long;
+  };
+  Meta* meta = nullptr;       // device (pool)
+  Meta* meta_host = nullptr;  // pinned mirror, read after the caller's sync
+  bool async_counts = false;
 };
+
+namespace gespmm {
+cudaError_t build_hot_bits(gespmm_plan_s* plan, const int* colind, int64_t H, cudaStream_t s);
+// The one-shot plan build with no host synchronization (gespmm_plan.cu).
+gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const int* colind,
+                                 bool check_colind, cudaStream_t s);
+std::string csr_error_message(int err, int64_t K);
+}  // namespace gespmm

@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
   };
 
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
-  int64_t t_begin = 0, t_end = P.n_items;
+  // the item count: on the device for plans built without a host sync
+  const int64_t n_items = P.n_items_dev ? *P.n_items_dev : P.n_items;
+  int64_t t_begin = 0, t_end = n_items;
   // a failed on-device colind check earlier on the stream (host entry point,
   // single- or multi-chunk): no item is gathered through an invalid colind
   if (P.abort_flag && *reinterpret_cast<const volatile int*>(P.abort_flag)) return;
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     int lo, hi, nr, re_long = 0;
     if (is_tile) {
       int r1, pend;
-      if (t + 1 < P.n_items) {
+      if (t + 1 < n_items) {
         const int4 nx = P.items[t + 1];
         r1 = nx.x;
         pend = nx.z;

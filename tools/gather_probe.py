@@ -1,6 +1,8 @@
 """Gather ceiling for the config-2 matrix: replays its colind stream through
 tools/libgather_probe.so (pure B-row gathers, N=64, L2 flushed before each
-rep) at several loads-in-flight / occupancy points.  Prints one JSON line."""
+rep) at several loads-in-flight / occupancy points: register loads, 16-byte
+cp.async rings and TMA bulk-copy rings (one cp.async.bulk per row, mbarrier
+completion).  Prints one JSON line."""
 import ctypes
 import json
 import os
@@ -24,6 +26,10 @@ def main():
     L.gather_probe_ring.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+    L.gather_probe_bulk.restype = ctypes.c_float
+    L.gather_probe_bulk.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_int64]
     L.gather_probe_pair.restype = ctypes.c_float
     L.gather_probe_pair.argtypes = L.gather_probe.argtypes
     dev = torch.device("cuda:0")
@@ -53,6 +59,15 @@ def main():
             ms = L.gather_probe_ring(B.data_ptr(), idx.data_ptr(), nnz, U, D, 256, bps, 5, sink.data_ptr(),
                                      flush.data_ptr(), flush.numel())
             out["results"].append({"stream": name, "ring": f"U{U}xD{D}", "warps_per_sm": 8 * bps, "ms": ms,
+                                   "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
+        # TMA bulk-copy ring: one single-lane cp.async.bulk per 256-byte row,
+        # mbarrier completion (VERDICT r1 Next 4)
+        for U, D, Wc, bps in ((16, 2, 8, 1), (16, 2, 8, 2), (16, 2, 8, 3), (16, 3, 8, 2), (32, 2, 4, 3),
+                              (32, 2, 8, 1), (8, 4, 8, 3), (16, 2, 4, 6)):
+            ms = L.gather_probe_bulk(B.data_ptr(), idx.data_ptr(), nnz, U, D, Wc, 256, bps, 5, sink.data_ptr(),
+                                     flush.data_ptr(), flush.numel())
+            out["results"].append({"stream": name, "bulk": f"U{U}xD{D}", "warps_per_sm": Wc * bps,
+                                   "rows_in_flight_per_sm": Wc * bps * U * (D - 1), "ms": ms,
                                    "gather_TBs": nnz * 256 / (ms * 1e-3) / 1e12 if ms > 0 else None})
     print(json.dumps(out))
 

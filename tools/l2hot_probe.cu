@@ -411,6 +411,10 @@ __global__ void __launch_bounds__(256, 1)
             const uint64_t pol = hot ? pl : pf;
             asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                          "l"(pol) : "memory");
+          } else if (MODE == 2) {  // the .ca form (L1 + L2) with the hint
+            const uint64_t pol = hot ? pl : pf;
+            asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                         "l"(pol) : "memory");
           } else {
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
           }
@@ -467,14 +471,15 @@ extern "C" float l2hot_probe_ldgsts(const float* B, const int* idx, int64_t nidx
   else if (vec == 4 && U == 4 && D == 4) X(4, 4, 4, MM);   \
   else if (vec == 4 && U == 8 && D == 2) X(8, 2, 4, MM);   \
   else if (vec == 4 && U == 4 && D == 6) X(4, 6, 4, MM);   \
+  else if (vec == 4 && U == 4 && D == 2) X(4, 2, 4, MM);   \
   else X(8, 2, 2, MM);
-  if (mode == 1) { ALL(SETA, 1) } else { ALL(SETA, 0) }
+  if (mode == 1) { ALL(SETA, 1) } else if (mode == 2) { ALL(SETA, 2) } else { ALL(SETA, 0) }
   for (int r = 0; r < reps + 1; ++r) {
     cudaDeviceSynchronize();
     if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
     cudaEventRecord(e0);
     for (int c0 = 0; c0 < 128; c0 += w) {
-      if (mode == 1) { ALL(RUN, 1) } else { ALL(RUN, 0) }
+      if (mode == 1) { ALL(RUN, 1) } else if (mode == 2) { ALL(RUN, 2) } else { ALL(RUN, 0) }
     }
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
@@ -488,6 +493,63 @@ extern "C" float l2hot_probe_ldgsts(const float* B, const int* idx, int64_t nidx
 #undef KB
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? best : -static_cast<float>(err);
+}
+
+// Hot rows pinned ahead of a plain (hint-free) LDGSTS ring: one pass puts every
+// line of the hot rows in L2 with evict_last priority (prefetch with a
+// policy), the ring runs, then a pass demotes them to evict_normal (so the
+// next launch's L2 flush really flushes them).
+__global__ void pin_rows(const float* __restrict__ B, const int* __restrict__ rows, int64_t n, int demote) {
+  uint64_t pl;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  const int64_t lines = n * 4;  // 512-byte rows = 4 lines
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < lines;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float* a = B + static_cast<int64_t>(rows[i >> 2]) * 128 + (i & 3) * 32;
+    if (demote) asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(a) : "memory");
+    else asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a) : "memory");
+  }
+}
+
+extern "C" float l2hot_probe_pinned(const float* B, const int* idx, int64_t nidx, const int* hot_rows, int64_t nhot,
+                                    int U, int D, int span, int warps_per_sm, int reps, float* sink, void* flush,
+                                    int64_t flush_bytes, float* pin_ms) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = 8 * D * U * 512;
+  const int grid = sms * (warps_per_sm / 8);
+  auto k = (U == 8 && D == 2) ? probe_ldgsts<8, 2, 4, 0> : probe_ldgsts<4, 4, 4, 0>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  float best = 1e30f, bpin = 0;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaDeviceSynchronize();
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    if (nhot > 0) pin_rows<<<sms * 4, 256>>>(B, hot_rows, nhot, 0);
+    cudaEventRecord(e1);
+    k<<<grid, 256, smem>>>(B, idx, nidx, span, 0, sink);
+    if (nhot > 0) pin_rows<<<sms * 4, 256>>>(B, hot_rows, nhot, 1);
+    cudaEventRecord(e2);
+    cudaEventSynchronize(e2);
+    float ms = 0, p = 0;
+    cudaEventElapsedTime(&ms, e0, e2);
+    cudaEventElapsedTime(&p, e0, e1);
+    if (r >= 1 && ms < best) {
+      best = ms;
+      bpin = p;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  if (pin_ms) *pin_ms = bpin;
   const cudaError_t err = cudaGetLastError();
   return err == cudaSuccess ? best : -static_cast<float>(err);
 }

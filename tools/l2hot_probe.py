@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--panel-u", type=int, default=8, help="rows in flight per warp (register replay)")
     ap.add_argument("--ldgsts", default="", help="LDGSTS ring configs vec:U:D:warps_per_sm,...")
     ap.add_argument("--bulk", default="", help="bulk-copy ring configs vec:U:D;... e.g. 2:16:2,4:8:4")
+    ap.add_argument("--pinned", default="", help="pinned hot set + plain LDGSTS ring, configs U:D:warps_per_sm")
     a = ap.parse_args()
     import bench
     from paper_2503_08946_b200 import workloads as W
@@ -55,6 +56,25 @@ def main():
     maxp = int(L.l2hot_max_persist())
     print(json.dumps({"nnz": col.numel(), "K": K, "max_persisting_l2": maxp,
                       "l2": torch.cuda.get_device_properties(0).L2_cache_size}), flush=True)
+    if a.pinned:
+        L.l2hot_probe_pinned.restype = ctypes.c_float
+        L.l2hot_probe_pinned.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                         ctypes.POINTER(ctypes.c_float)]
+        for mb in [0] + [int(x) for x in a.hot_mb.split(",")]:
+            H = (mb << 20) // 512
+            hot = order[:H].to(torch.int32).contiguous()
+            for cfg in a.pinned.split(","):
+                U, D, wps = (int(x) for x in cfg.split(":"))
+                pin = ctypes.c_float(0)
+                ms = L.l2hot_probe_pinned(B.data_ptr(), col.data_ptr(), col.numel(), hot.data_ptr(), H, U, D,
+                                          a.span, wps, a.reps, sink.data_ptr(), flush.data_ptr(), flush.numel(),
+                                          ctypes.byref(pin))
+                print(json.dumps({"pinned": cfg, "hot_mb": mb, "hot_share": round(float(cum[H - 1]), 4) if H else 0,
+                                  "ms_incl_pin_and_demote": round(ms, 3), "pin_ms": round(pin.value, 3)}),
+                      flush=True)
+        return
     if a.panels:
         L.l2hot_probe_panels.restype = ctypes.c_float
         L.l2hot_probe_panels.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
