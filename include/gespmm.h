@@ -225,11 +225,6 @@ gespmm_status_t gespmm_set_schedule_override(int mode);
  * in [2, 256].  Results are identical for every value (rows stay whole).
  * Test/tuning knob; not thread-safe. */
 gespmm_status_t gespmm_set_tile_work_override(int32_t units);
-/* L2 hot set of B rows: -1 = automatic (GESPMM_HOT env,
- * default on when the 128-column tile's B slab is >= 4x L2), 0 = off, 1 = on
- * at any size.  Only L2 cache policies change; results are identical.
- * Test/tuning knob; not thread-safe. */
-gespmm_status_t gespmm_set_hot_override(int mode);
 /* The panel width gespmm_plan_execute uses for a K-row B with N columns: one
  * kernel launch per panel, ceil(N / width) launches per execute. */
 int64_t gespmm_panel_width(int64_t K, int64_t N);

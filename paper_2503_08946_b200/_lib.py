@@ -25,7 +25,7 @@ EXPORTS = [
     "gespmm_plan_create", "gespmm_plan_execute", "gespmm_plan_execute_rows", "gespmm_plan_destroy",
     "gespmm_plan_execute_peers", "gespmm_ipc_get_handle", "gespmm_ipc_open_handle", "gespmm_ipc_close_handle", "gespmm_plan_get_info",
     "gespmm_variant_name", "gespmm_set_variant_override", "gespmm_set_panel_override",
-    "gespmm_panel_width", "gespmm_set_schedule_override", "gespmm_set_tile_work_override", "gespmm_set_hot_override", "gespmm_partition_rows",
+    "gespmm_panel_width", "gespmm_set_schedule_override", "gespmm_set_tile_work_override", "gespmm_partition_rows",
     "gespmm_rmat_csr", "gespmm_uniform_fill", "gespmm_coo_to_csr", "gespmm_csr_transpose",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
     "gespmm_sharded_spmm_chunked", "gespmm_sharded_spmm_ex", "gespmm_comm_wait",
@@ -89,7 +89,6 @@ def load():
         "gespmm_panel_width": ([_i64, _i64], _i64),
         "gespmm_set_schedule_override": ([_int], _int),
         "gespmm_set_tile_work_override": ([ctypes.c_int32], _int),
-        "gespmm_set_hot_override": ([_int], _int),
         "gespmm_partition_rows": ([_i64, _vp, _int, _vp], _int),
         "gespmm_rmat_csr": ([_int, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                              ctypes.c_uint64, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp], _int),

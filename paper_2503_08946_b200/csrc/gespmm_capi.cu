@@ -126,7 +126,7 @@ Variant pick_variant(int64_t N, const float* B, int64_t ldb, const float* C, int
 }
 
 // Plan-owned device buffers (items, partials, counters, work counters, the
-// hot set) come from the device's stream-ordered pool (cudaMallocAsync on the
+// one-shot plan's meta) come from the device's stream-ordered pool (cudaMallocAsync on the
 // plan's stream; the pool keeps its memory mapped, gespmm_plan.cu
 // keep_pool_resident), so a fresh plan costs no cudaMalloc round trip
 // (config 2: 1.46 ms per fresh Plan with cudaMalloc); grow-only, released with
@@ -244,45 +244,6 @@ int64_t panel_width(int64_t K, int64_t N) {
   return w < N ? w : N;
 }
 
-// L2 hot-set size in B rows for one launch (0: off).  On when the gathered B
-// slab (K x n fp32) is at least GESPMM_HOT_MIN_X (4) times the L2 size, the
-// tile is the 128-column register tile (512-byte rows) and 32-bit offsets
-// leave bit 31 free (K*ldb <= 2^31); H = GESPMM_HOT_MB (64 MB) of rows.
-// GESPMM_HOT=0 disables it.  Measured on config 5's column stream
-// (tools/l2hot_probe.cu, profiles/r2_l2hot_probe_config5.jsonl): 64 MB of hot
-// rows evict_last + cold rows evict_first 44.1 -> 39.1 ms (register gathers,
-// 4 rows in flight per warp); a persisting access-policy window on a compact
-// copy of the hot rows, or the hot rows alone evict_last, gained less.
-int g_hot_override = -1;  // gespmm_set_hot_override: -1 auto, 0 off, 1 any size
-int64_t hot_rows(int64_t K, int64_t n, int64_t ldb, const Variant& v) {
-  static const int env_mode = [] {  // measured slower than the ring: off by default
-    const char* e = std::getenv("GESPMM_HOT");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int mode = g_hot_override == 0 ? 0 : g_hot_override == 1 ? 2 : env_mode;
-  static const int64_t mb = [] {
-    const char* e = std::getenv("GESPMM_HOT_MB");
-    const long long x = e ? std::atoll(e) : 64;
-    return static_cast<int64_t>(x > 0 ? x : 64);
-  }();
-  static const int64_t min_x = [] {
-    const char* e = std::getenv("GESPMM_HOT_MIN_X");
-    const long long x = e ? std::atoll(e) : 4;
-    return static_cast<int64_t>(x > 0 ? x : 4);
-  }();
-  if (mode == 0 || v.pair || v.vec != 4 || v.cwm != 1 || n <= 0) return 0;
-  if (K * ldb > (int64_t(1) << 31)) return 0;
-  static int64_t l2 = [] {
-    int dev = 0, b = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&b, cudaDevAttrL2CacheSize, dev);
-    return static_cast<int64_t>(b > 0 ? b : (126 << 20));
-  }();
-  if (mode != 2 && K * n * 4 < min_x * l2) return 0;  // GESPMM_HOT=2: any size (tests)
-  const int64_t H = (mb << 20) / (n * 4);
-  return H < 1 ? 1 : H;
-}
-
 // The launches of one execute (one per column panel), optionally restricted
 // to the item range *range (device memory) with an on-device abort flag.
 gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* rowptr,
@@ -363,19 +324,6 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     p.n_peers = n_peers;
     p.peer_shift = peer_shift;
     for (int q = 0; q < n_peers; ++q) p.peers[q] = peers[q] + c0;  // this panel's columns
-    // L2 hot set (gespmm_hot.cu): B many times larger than L2, 512-byte rows
-    // (the 128-column register tile), whole-plan launches only; built once
-    // per plan and size, on the stream (no host sync)
-    p.hot_bits = nullptr;
-    p.hot_K = static_cast<int>(plan->K);
-    const int64_t H = hot_rows(plan->K, n, ldb, v);
-    if (H > 0 && !range && !abort_flag && n_peers == 0 && plan->nnz > 0) {
-      if (plan->hot_key != H) {
-        cudaError_t he = build_hot_bits(plan, colind, H, s);
-        if (he != cudaSuccess) return cuda_fail(he, "L2 hot set");
-      }
-      p.hot_bits = plan->hot_bits;
-    }
     cudaError_t e = launch_spmm(op, v, p, s);
     if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
   }
@@ -588,7 +536,6 @@ gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
   if (plan->items) cudaFree(plan->items);
   if (plan->partials) cudaFree(plan->partials);
   if (plan->counters) cudaFree(plan->counters);
-  if (plan->hot_bits) cudaFree(plan->hot_bits);
   if (plan->meta) cudaFree(plan->meta);
   if (plan->meta_host) cudaFreeHost(plan->meta_host);
   delete plan;
@@ -869,12 +816,6 @@ int64_t gespmm_panel_width(int64_t K, int64_t N) { return N < 1 ? 0 : panel_widt
 gespmm_status_t gespmm_set_schedule_override(int mode) {
   if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: schedule mode -1/0/1");
   g_schedule_override = mode;
-  return GESPMM_OK;
-}
-
-gespmm_status_t gespmm_set_hot_override(int mode) {
-  if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: hot mode -1/0/1");
-  g_hot_override = mode;
   return GESPMM_OK;
 }
 

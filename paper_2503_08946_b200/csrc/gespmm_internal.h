@@ -115,10 +115,6 @@ struct KParams {
   int64_t peer_shift;
   // dynamic item distribution: one counter per column block, zero at launch
   unsigned long long* work_ctr;
-  // L2 hot set (gespmm_hot.cu; nullptr: off): bit c set = column c's B row
-  // is gathered with L2 evict_last, every other row with evict_first
-  const uint32_t* hot_bits;
-  int hot_K;
 };
 
 // GESPMM_TRACE=1: phase timings of the host entry point and the plan build on
@@ -171,11 +167,6 @@ struct gespmm_plan_s {
   int64_t counter_ints = 0;
   int tile_work = gespmm::kTileWork;
   int device = 0;
-  // L2 hot set of B rows (gespmm_hot.cu), built at the first execute that
-  // wants one; hot_key = its size H in rows (-1: none / stale after re-plan)
-  uint32_t* hot_bits = nullptr;
-  int64_t hot_words = 0;
-  int64_t hot_key = -1;
   // build_plan_async (the one-shot entry point): counts and the CSR error
   // bits stay on the device (meta); n_items / n_segs hold upper bounds and
   // every launch reads the true count and aborts on an error bit
@@ -189,7 +180,6 @@ struct gespmm_plan_s {
 };
 
 namespace gespmm {
-cudaError_t build_hot_bits(gespmm_plan_s* plan, const int* colind, int64_t H, cudaStream_t s);
 // The one-shot plan build with no host synchronization (gespmm_plan.cu).
 gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const int* colind,
                                  bool check_colind, cudaStream_t s);

@@ -334,21 +334,9 @@ struct Ring {
   static constexpr bool kSupported = CWM == 1 && VEC >= 2;  // N = 64 / 128 column tiles
 };
 
-// HOT (register path, 32-bit offsets): the L2 hot set (gespmm_hot.cu) -- the
-// pre-scale pass tags each staged offset with its column's hot bit (bit 31;
-// the launch guarantees K*ldb <= 2^31), and each gather picks evict_last for
-// a hot row, evict_first for a cold one.  Addresses and arithmetic unchanged.
-#ifndef GESPMM_HOT_U
-#define GESPMM_HOT_U 4  // rows per batch of the hot-set instantiation
-#endif
-#ifndef GESPMM_HOT_MINB
-#define GESPMM_HOT_MINB 4  // its CTAs per SM (register cap)
-#endif
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS, bool HOT = false>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32,
-                                  RING ? 3 : HOT ? GESPMM_HOT_MINB : MinBlocks<VEC * CWM>::value)
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC * CWM>::value)
     spmm_kernel(const KParams P) {
-  static_assert(!HOT || (OFF32 && !RING), "hot set: register gathers with 32-bit offsets");
   using SR = Semiring<OP>;
   // sum/mean: two FMA chains per row (even/odd offsets from the row start),
   // held in accumulator slots by absolute position parity (batches are
@@ -357,7 +345,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   // even chain).  max/min: one chain in slot 0.
   constexpr bool TWO = SR::kFma2;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
-  constexpr int U = RING ? Ring<VEC, CWM>::U : HOT ? GESPMM_HOT_U : Pipe<CPL>::U;  // gathers per batch
+  constexpr int U = RING ? Ring<VEC, CWM>::U : Pipe<CPL>::U;  // gathers per batch
   constexpr int FB = RING ? 0 : CPL == 1 ? GESPMM_FAST_VEC1 : CPL == 2 ? GESPMM_FAST_VEC2 : 0;  // in-row fast batch
   using RG = Ring<VEC, CWM>;
   static_assert(!RING || RG::kSupported, "ring mode: CWM == 1, VEC >= 2");
@@ -452,19 +440,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
     }
   };
   const uint64_t bpol = GESPMM_BHINT ? policy_evict_last() : 0;
-  const uint64_t cpol = HOT ? policy_evict_first() : 0;
   auto gather = [&](float (&d)[CWM][VEC], int x) {
     if (GESPMM_ABL_NOGATHER) {  // ablation builds only
 #pragma unroll
       for (int w = 0; w < CWM; ++w)
 #pragma unroll
         for (int k = 0; k < VEC; ++k) d[w][k] = __int_as_float(x + k);
-      return;
-    }
-    if constexpr (HOT) {  // bit 31: hot row (L2 evict_last), else evict_first
-      const uint64_t pol = x < 0 ? bpol : cpol;
-#pragma unroll
-      for (int w = 0; w < CWM; ++w) gather_off<VEC>(d[w], bw[w], static_cast<uint32_t>(x) & 0x7fffffffu, pol);
       return;
     }
 #pragma unroll
@@ -624,22 +605,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
       const uint32_t ldb32 = static_cast<uint32_t>(ldb);
       const int pad = hi - sbase, head = lo - sbase;
       auto keep = [&](int j) { return j >= head && j < pad; };
-      // HOT: the column's hot bit into bit 31 of its offset (an out-of-range
-      // column never reads the bitmap)
-      auto tag = [&](int col) -> uint32_t {
-        if constexpr (HOT) {
-          if (static_cast<uint32_t>(col) >= static_cast<uint32_t>(P.hot_K)) return 0u;
-          return (__ldg(P.hot_bits + (col >> 5)) << (31 - (col & 31))) & 0x80000000u;
-        } else {
-          return 0u;
-        }
-      };
       for (int i = 4 * lane; i < send - sbase; i += 128) {
         int4 c = *reinterpret_cast<int4*>(sc + i);
-        c.x = keep(i + 0) ? static_cast<int>((static_cast<uint32_t>(c.x) * ldb32) | tag(c.x)) : 0;
-        c.y = keep(i + 1) ? static_cast<int>((static_cast<uint32_t>(c.y) * ldb32) | tag(c.y)) : 0;
-        c.z = keep(i + 2) ? static_cast<int>((static_cast<uint32_t>(c.z) * ldb32) | tag(c.z)) : 0;
-        c.w = keep(i + 3) ? static_cast<int>((static_cast<uint32_t>(c.w) * ldb32) | tag(c.w)) : 0;
+        c.x = keep(i + 0) ? static_cast<int>(static_cast<uint32_t>(c.x) * ldb32) : 0;
+        c.y = keep(i + 1) ? static_cast<int>(static_cast<uint32_t>(c.y) * ldb32) : 0;
+        c.z = keep(i + 2) ? static_cast<int>(static_cast<uint32_t>(c.z) * ldb32) : 0;
+        c.w = keep(i + 3) ? static_cast<int>(static_cast<uint32_t>(c.w) * ldb32) : 0;
         *reinterpret_cast<int4*>(sc + i) = c;
       }
       __syncwarp();
@@ -899,7 +870,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
 #undef GESPMM_NEXT_ITEM
 }
 
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS = false, bool HOT = false>
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS = false>
 cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks == 0) return cudaSuccess;
@@ -912,9 +883,9 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (RING)
-      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS, HOT>,
+      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS, HOT>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS>,
                                                   kWarpsPerBlock * 32, smem);
     cached_slots = sms * (per_sm > 0 ? per_sm : 1);
     cached_dev = dev;
@@ -922,7 +893,7 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   const int64_t slots = (cached_slots + p.ncb - 1) / p.ncb;
   if (blocks > slots) blocks = slots;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(p.ncb), 1);
-  spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS, HOT><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
+  spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -936,9 +907,6 @@ cudaError_t launch_off(const Variant& v, const KParams& p, cudaStream_t s) {
     if (v.vec == 2 && v.cwm == 1) return launch_t<OP, 2, 1, OFF32, false, true>(p, s);
     if (v.vec == 1 && v.cwm == 2) return launch_t<OP, 1, 2, OFF32, false, true>(p, s);
     return launch_t<OP, 1, 1, OFF32, false, true>(p, s);
-  }
-  if constexpr (OFF32) {  // L2 hot set (gespmm_hot.cu): 128-column register tile
-    if (p.hot_bits && v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, true, false, false, true>(p, s);
   }
   const bool ring = v.ring && OFF32 && p.ldb % 4 == 0 && p.N % 4 == 0 &&
                     reinterpret_cast<uintptr_t>(p.B) % 16 == 0;

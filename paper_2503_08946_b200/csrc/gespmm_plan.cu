@@ -289,8 +289,7 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
                            bool check_colind, cudaStream_t s) {
   NvtxRange nvtx("gespmm:plan_build");
   keep_pool_resident();
-  plan->hot_key = -1;
-  plan->async_counts = false;  // a re-planned structure: the hot set is rebuilt on demand
+  plan->async_counts = false;
   const int64_t M = plan->M;
   const int M32 = static_cast<int>(M);
   const int nnz32 = static_cast<int>(plan->nnz);
@@ -410,7 +409,6 @@ gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const i
                                  bool check_colind, cudaStream_t s) {
   NvtxRange nvtx("gespmm:plan_build_async");
   keep_pool_resident();
-  plan->hot_key = -1;
   const int64_t M = plan->M;
   const int M32 = static_cast<int>(M);
   const int nnz32 = static_cast<int>(plan->nnz);

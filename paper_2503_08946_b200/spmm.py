@@ -319,12 +319,6 @@ def set_tile_work_override(units: int = 0) -> None:
     _lib.check(_L.gespmm_set_tile_work_override(int(units)))
 
 
-def set_hot_override(mode: int = -1) -> None:
-    """L2 hot set of B rows: -1 automatic, 0 off, 1 on at any size; results
-    never depend on it.  Test/tuning knob (gespmm_set_hot_override)."""
-    _lib.check(_L.gespmm_set_hot_override(int(mode)))
-
-
 def set_panel_override(cols: int = -1) -> None:
     """Column-panel width: -1 heuristic, 0 never split, > 0 forced width."""
     _lib.check(_L.gespmm_set_panel_override(int(cols)))

@@ -915,69 +915,6 @@ def test_comm_wait_timeout_aborts_instead_of_hanging(cuda):
 
 
 @pytest.mark.parametrize("op", OPS)
-def test_l2_hot_set_forced_bit_exact(cuda, oracle_mod, op):
-    """The L2 hot set (gespmm_hot.cu; hot rows evict_last, cold rows
-    evict_first, tagged in bit 31 of the staged offsets) forced on a small
-    product: bit-identical to the twin and to hot-set-off, for a skewed
-    column distribution (so the hot set is a proper subset), unaligned vals
-    (4-byte staging), accumulate, long rows and a second N (re-sized set)."""
-    import torch
-
-    from paper_2503_08946_b200.spmm import Plan, set_hot_override
-
-    rng = np.random.default_rng(70)
-    M, K = 6_000, 40_000
-    deg = np.minimum((rng.pareto(1.1, M) * 6).astype(np.int64), 3_000)
-    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
-    nnz = int(rowptr[-1])
-    colind = np.minimum((rng.pareto(0.8, nnz) * 50).astype(np.int64), K - 1).astype(np.int32)
-    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
-    try:
-        for N in (128, 100):
-            B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
-            C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
-            rp, ci, Bt = to_dev(cuda, rowptr, colind, B)
-            vbuf = torch.empty(nnz + 1, device=cuda)
-            vbuf[1:] = torch.as_tensor(vals, device=cuda)
-            vv = vbuf[1:]  # 4-byte aligned only
-            plan = Plan(rp, ci, K)
-            outs = {}
-            for hot in (1, 0):
-                set_hot_override(hot)
-                C = torch.as_tensor(C0, device=cuda).clone()
-                plan.execute(vv, Bt, op, out=C, accumulate=True)
-                outs[hot] = C.cpu().numpy()
-            want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=True, C0=C0, seg_len=SEG)
-            np.testing.assert_array_equal(outs[1], want)
-            np.testing.assert_array_equal(outs[0], want)
-    finally:
-        set_hot_override(-1)
-
-
-def test_l2_hot_set_automatic_on_large_b(cuda, oracle_mod):
-    """B = 1.2M x 128 fp32 (614 MB, > 4x L2): the hot set turns on by itself;
-    sum and max bit-exact to the twin on sampled rows (the full-size R-MAT
-    configs 4/5 run it too, test_full_size_configs_sampled_bit_exact)."""
-    import torch
-
-    from paper_2503_08946_b200 import workloads as W
-    from paper_2503_08946_b200.spmm import Plan
-
-    K, N = 1_200_000, 128
-    csr = W.rmat_csr_gpu(20, 4 * 2**20, seed=9, device=cuda)
-    # columns spread over the wider B: col * 1.144 (keeps R-MAT's skew)
-    colind = (csr.colind.long() * K // csr.K).to(torch.int32)
-    csr = W.Csr(csr.rowptr, colind, csr.vals, csr.M, K)
-    B = W.dense_gpu(K, N, seed=4, device=cuda)
-    plan = Plan(csr.rowptr, csr.colind, K)
-    C = torch.empty((csr.M, N), device=cuda)
-    for op in ("sum", "max"):
-        plan.execute(csr.vals, B, op, out=C)
-        torch.cuda.synchronize()
-        sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=1500, tag="hot-auto")
-
-
-@pytest.mark.parametrize("op", OPS)
 def test_64bit_b_offsets(cuda, oracle_mod, op):
     """K * ldb > 2^32: the kernel's 64-bit B-row addressing path (staged 32-bit
     offsets would overflow).  B is a strided view (ldb ~ 7.2 M floats) into a
