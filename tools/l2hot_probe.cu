@@ -553,3 +553,145 @@ extern "C" float l2hot_probe_pinned(const float* B, const int* idx, int64_t nidx
   const cudaError_t err = cudaGetLastError();
   return err == cudaSuccess ? best : -static_cast<float>(err);
 }
+
+// TMA gather4 ring (round 2): B rows (512 B, N = 128) fetched four at a time
+// by one elected lane with cp.async.bulk.tensor.2d.tile::gather4 into a
+// per-warp shared-memory ring (S stages x G gather4 = 4G rows per stage),
+// mbarrier completion.  MODE 1: the gather4 carries an L2 cache hint --
+// evict_last when any of its 4 rows is hot, evict_first otherwise.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+template <int S, int G, int MODE>
+__global__ void __launch_bounds__(256, 1) probe_tma(const __grid_constant__ CUtensorMap tm, const int* __restrict__ idx,
+                                                  int64_t nidx, int span, float* sink) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int RB = 512, STAGE = G * 4 * RB;
+  __shared__ __align__(8) uint64_t bar[8][S];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* ring = smraw + wib * S * STAGE;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t pl, pf;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  if (lane < S) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][lane]));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t phase = 0;
+  float a0 = 0.f;
+  constexpr int PER = 4 * G;
+  for (int64_t s0 = warp * span; s0 < nidx; s0 += nw * span) {
+    const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
+    const int nb = static_cast<int>((s1 - s0) / PER);  // whole stages only (the tail is skipped: a probe)
+    auto issue = [&](int k) {
+      if (k >= nb || lane != 0) return;
+      const int d = k % S;
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(STAGE) : "memory");
+      const int* ip = idx + s0 + static_cast<int64_t>(k) * PER;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int e0 = __ldg(ip + 4 * g), e1 = __ldg(ip + 4 * g + 1), e2 = __ldg(ip + 4 * g + 2),
+                  e3 = __ldg(ip + 4 * g + 3);
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(ring + d * STAGE + g * 4 * RB));
+        const int r0 = e0 & 0x7fffffff, r1 = e1 & 0x7fffffff, r2 = e2 & 0x7fffffff, r3 = e3 & 0x7fffffff;
+        if (MODE == 1) {
+          const uint64_t pol = (e0 | e1 | e2 | e3) < 0 ? pl : pf;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+              "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(b), "l"(pol)
+              : "memory");
+        } else {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+              "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(b)
+              : "memory");
+        }
+      }
+    };
+    for (int k = 0; k < S - 1; ++k) issue(k);
+    for (int k = 0; k < nb; ++k) {
+      issue(k + S - 1);
+      const int d = k % S;
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
+      const uint32_t par = (phase >> d) & 1u;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(b), "r"(par) : "memory");
+      phase ^= 1u << d;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const float4 v = reinterpret_cast<const float4*>(ring + d * STAGE + u * RB)[lane];
+        a0 += v.x + v.y + v.z + v.w;
+      }
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+  }
+  if (a0 == 1234.5f) sink[0] = a0;
+}
+
+extern "C" float l2hot_probe_tma(const float* B, int64_t K, const int* idx, int64_t nidx, int mode, int S, int G,
+                                 int warps_per_sm, int span, int reps, float* sink, void* flush, int64_t flush_bytes) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+          cudaSuccess || !encode)
+    return -1.f;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(K)};
+  cuuint64_t strides[1] = {128 * 4};
+  cuuint32_t box[2] = {128, 1};
+  cuuint32_t es[2] = {1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -3.f;
+  const int smem = 8 * S * G * 4 * 512;
+  const int grid = sms * (warps_per_sm / 8);
+#define TMA_ALL(X)                                   \
+  if (S == 4 && G == 1) { X(4, 1) }                  \
+  else if (S == 3 && G == 2) { X(3, 2) }             \
+  else if (S == 2 && G == 2) { X(2, 2) }             \
+  else if (S == 6 && G == 1) { X(6, 1) }             \
+  else return -2.f;
+#define TMA_SET(a, b)                                                                                        \
+  cudaFuncSetAttribute(probe_tma<a, b, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);              \
+  cudaFuncSetAttribute(probe_tma<a, b, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+#define TMA_RUN(a, b)                                                                              \
+  if (mode == 1) probe_tma<a, b, 1><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);              \
+  else probe_tma<a, b, 0><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);
+  TMA_ALL(TMA_SET)
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaDeviceSynchronize();
+    if (flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+    cudaEventRecord(e0);
+    TMA_ALL(TMA_RUN)
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 1 && ms < best) best = ms;
+  }
+#undef TMA_ALL
+#undef TMA_SET
+#undef TMA_RUN
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? best : -static_cast<float>(err);
+}

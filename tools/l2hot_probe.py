@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--ldgsts", default="", help="LDGSTS ring configs vec:U:D:warps_per_sm,...")
     ap.add_argument("--bulk", default="", help="bulk-copy ring configs vec:U:D;... e.g. 2:16:2,4:8:4")
     ap.add_argument("--pinned", default="", help="pinned hot set + plain LDGSTS ring, configs U:D:warps_per_sm")
+    ap.add_argument("--tma", default="", help="TMA gather4 ring configs S:G:warps_per_sm, e.g. 4:1:24,3:2:16")
     a = ap.parse_args()
     import bench
     from paper_2503_08946_b200 import workloads as W
@@ -56,6 +57,26 @@ def main():
     maxp = int(L.l2hot_max_persist())
     print(json.dumps({"nnz": col.numel(), "K": K, "max_persisting_l2": maxp,
                       "l2": torch.cuda.get_device_properties(0).L2_cache_size}), flush=True)
+    if a.tma:
+        L.l2hot_probe_tma.restype = ctypes.c_float
+        L.l2hot_probe_tma.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        for mb in [0] + [int(x) for x in a.hot_mb.split(",")]:
+            H = (mb << 20) // 512
+            hotflag = torch.zeros(K, dtype=torch.bool, device=dev)
+            if H:
+                hotflag[order[:H]] = True
+            flagged = col | (hotflag[col].to(torch.int32) << 31)
+            for cfg in a.tma.split(","):
+                S_, G_, wps = (int(x) for x in cfg.split(":"))
+                ms = L.l2hot_probe_tma(B.data_ptr(), K, flagged.data_ptr(), col.numel(), 1 if mb else 0, S_, G_, wps,
+                                       a.span, a.reps, sink.data_ptr(), flush.data_ptr(), flush.numel())
+                print(json.dumps({"tma": cfg, "mode": 1 if mb else 0, "hot_mb": mb,
+                                  "hot_share": round(float(cum[H - 1]), 4) if H else 0, "ms": round(ms, 3)}),
+                      flush=True)
+            del flagged
+        return
     if a.pinned:
         L.l2hot_probe_pinned.restype = ctypes.c_float
         L.l2hot_probe_pinned.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
