@@ -618,12 +618,17 @@ class Measure:
         U, G = algorithmic_bytes(self.M_loc, self.K, self.N, self.nnz_loc)
         peak, peak_src = peaks()
         achieved = U / (t_mean * 1e-3) / 1e9
+        ncu = ncu_record("ncu_metrics.json", self.name, self.args.op, self.world)
         return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak,
                 "traffic": ncu_record("traffic.json", self.name, self.args.op, self.world),
+                # the measured side of SURVEY 8(d): ncu DRAM bytes / duration of the
+                # same kernel against the same peak (the >= 70 % HBM target)
+                "dram_frac_ncu": (ncu["dram_GBs"] / peak) if ncu and ncu.get("dram_GBs") else None,
+                "l2_hit_pct_ncu": ncu.get("l2_hit_pct") if ncu else None,
                 "bytes_model": f"U = 4(M+1) + 8nnz + 4KN + 4MN = {U} B per launch",
                 "peak_source": peak_src, "gather_bytes_G": G, "gather_GBs": G / (t_mean * 1e-3) / 1e9,
-                "ncu": ncu_record("ncu_metrics.json", self.name, self.args.op, self.world)}
+                "ncu": ncu}
 
     def gather_ceiling(self, t_mean):
         """tools/gather_probe.cu replays this matrix's colind as B-row gathers

@@ -542,14 +542,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     int lo, hi, nr, re_long = 0;
     if (is_tile) {
       int r1, pend;
-      if (t + 1 < n_items) {
-        const int4 nx = P.items[t + 1];
-        r1 = nx.x;
-        pend = nx.z;
-      } else {
-        r1 = P.M;
-        pend = P.nnz;
-      }
+      // the next item (the plan's sentinel {M, -1, nnz} after the last one)
+      const int4 nx = P.items[t + 1];
+      r1 = nx.x;
+      pend = nx.z;
       nr = r1 - it.x;  // 1 <= nr <= kTileMaxRows (plan invariant)
       lo = it.z;
       hi = pend;

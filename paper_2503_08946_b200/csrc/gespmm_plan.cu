@@ -114,12 +114,18 @@ __global__ void k_totals(const uint64_t* packed, const uint64_t* E, const int* c
   out->n_long = err[1];
 }
 
+// items[n_items] = {M, -1, nnz, 0}: a tile "starting" at row M, position
+// nnz -- so every item's end is items[t + 1] with no bound check in the
+// kernel (the last real tile ends at row M / position nnz).
+__global__ void k_sentinel(int4* items, int64_t n, int M, int nnz) { items[n] = make_int4(M, -1, nnz, 0); }
+
 // The async build's counts (one thread): n_items, n_segs, error bits.
 constexpr int kErrItemCap = 16;  // more items than the bound (invalid rowptr only)
 __global__ void k_meta(const uint64_t* packed, const uint64_t* E, const int* cnt, const int* pos, int M,
-                       const int* err, int64_t cap, gespmm_plan_s::Meta* out) {
+                       int nnz, const int* err, int64_t cap, int4* items, gespmm_plan_s::Meta* out) {
   const int64_t n = static_cast<int64_t>(pos[M - 1]) + cnt[M - 1];
   out->n_items = n < cap ? n : cap;
+  items[out->n_items] = make_int4(M, -1, nnz, 0);  // the sentinel (k_sentinel)
   out->n_segs = static_cast<int64_t>(E[M - 1] >> kPackShift) + static_cast<int64_t>(packed[M - 1] >> kPackShift);
   out->err = err[0] | (n > cap ? kErrItemCap : 0);
   out->n_long = err[1];
@@ -370,7 +376,7 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
     if (plan->items) cudaFree(plan->items);
     plan->items = nullptr;
     plan->items_cap = 0;
-    const int64_t cap = plan->n_items > 0 ? plan->n_items : 1;
+    const int64_t cap = plan->n_items + 1;  // + the sentinel
     ce = cudaMallocAsync(&plan->items, static_cast<size_t>(cap) * sizeof(int4), s);
     if (ce != cudaSuccess) {
       cudaFreeAsync(arena, s);
@@ -379,7 +385,8 @@ gespmm_status_t build_plan(gespmm_plan_s* plan, const int* rowptr, const int* co
     plan->items_cap = cap;
   }
   tr.mark("totals D2H + items alloc", s);
-  k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, tw, plan->items, plan->items_cap);
+  k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, tw, plan->items, plan->n_items);
+  k_sentinel<<<1, 1, 0, s>>>(plan->items, plan->n_items, M32, nnz32);
   ce = cudaGetLastError();
   cudaFreeAsync(arena, s);
   tr.mark("emit", s);
@@ -431,13 +438,13 @@ gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const i
     if (plan->nnz != 0) return fail(GESPMM_CSR_INVALID, "invalid csr: rowPtr end differs from nnz of colInd");
     return GESPMM_OK;
   }
-  if (!plan->items || plan->items_cap < ub_items) {
+  if (!plan->items || plan->items_cap < ub_items + 1) {
     if (plan->items) cudaFree(plan->items);
     plan->items = nullptr;
     plan->items_cap = 0;
-    ce = cudaMallocAsync(&plan->items, static_cast<size_t>(ub_items) * sizeof(int4), s);
+    ce = cudaMallocAsync(&plan->items, static_cast<size_t>(ub_items + 1) * sizeof(int4), s);
     if (ce != cudaSuccess) return cuda_fail(ce, "plan items");
-    plan->items_cap = ub_items;
+    plan->items_cap = ub_items + 1;
   }
   uint64_t *packed = nullptr, *E = nullptr;
   int *cnt = nullptr, *pos = nullptr, *err = nullptr;
@@ -481,7 +488,7 @@ gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const i
   tb = tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pos, M32, s);
   k_emit<<<blocks, 256, 0, s>>>(rowptr, packed, E, pos, M32, tw, plan->items, ub_items);
-  k_meta<<<1, 1, 0, s>>>(packed, E, cnt, pos, M32, err, ub_items, plan->meta);
+  k_meta<<<1, 1, 0, s>>>(packed, E, cnt, pos, M32, nnz32, err, ub_items, plan->items, plan->meta);
   ce = cudaGetLastError();
   cudaFreeAsync(arena, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "plan build");

@@ -50,7 +50,7 @@ def panel_bounds(N: int, panels: int):
     """Column panels [c0, c1) of B for the overlapped broadcast: `panels`
     near-equal widths, multiples of 32 columns where N allows (one warp row
     per panel row), never empty."""
-    panels = max(1, min(int(panels), max(1, N // 32) if N >= 32 else 1))
+    panels = max(1, min(int(panels), -(-N // 32)))  # at most one panel per 32 columns
     step = -(-N // panels)
     if N >= 32:
         step = -(-step // 32) * 32

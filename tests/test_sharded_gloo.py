@@ -105,3 +105,21 @@ def test_sharded_gloo_bit_identical(world, oracle_mod):
                 np.testing.assert_array_equal(out[op + "96"], want96)
     b = results[0][2]
     assert b[0] == 0 and b[-1] == len(rowptr) - 1 and all(x <= y for x, y in zip(b, b[1:]))
+
+
+@pytest.mark.parametrize("N,panels,want", [(128, 4, [(0, 32), (32, 64), (64, 96), (96, 128)]),
+                                           (128, 3, [(0, 64), (64, 128)]),
+                                           (80, 2, [(0, 64), (64, 80)]), (80, 4, [(0, 32), (32, 64), (64, 80)]),
+                                           (16, 4, [(0, 16)]), (100, 1, [(0, 100)]), (256, 99, None)])
+def test_panel_bounds(N, panels, want):
+    """Column panels of the overlapped B broadcast: cover [0, N) in order, no
+    empty panel, widths multiples of 32 except the last (one warp row each)."""
+    from paper_2503_08946_b200.sharded import panel_bounds
+
+    pb = panel_bounds(N, panels)
+    if want is not None:
+        assert pb == want
+    assert pb[0][0] == 0 and pb[-1][1] == N
+    assert all(a < b for a, b in pb) and all(pb[i][1] == pb[i + 1][0] for i in range(len(pb) - 1))
+    assert all((b - a) % 32 == 0 for a, b in pb[:-1])
+    assert len(pb) <= max(1, panels)
