@@ -223,19 +223,32 @@ gespmm_status_t gespmm_sharded_spmm_ex(void* comm, int world, int rank, int root
     return x;
   };
   if (!plan && world > 1) {
+    // host words in pinned memory: a copy to or from pageable memory can block
+    // inside cudaMemcpyAsync -- forever, if a peer never joins the all-reduce --
+    // before the bounded wait below could see it.  [0] = this rank's status,
+    // [1] = the agreed (max) status.
+    static thread_local int* words = [] {
+      int* p = nullptr;
+      return cudaMallocHost(reinterpret_cast<void**>(&p), 2 * sizeof(int)) == cudaSuccess ? p : nullptr;
+    }();
+    if (!words) return done(gespmm::fail(GESPMM_CUDA_ERROR, "status agreement: pinned host words"));
+    words[0] = st == GESPMM_OK ? 0 : static_cast<int>(st);
+    words[1] = 0;
     int* flag = nullptr;
     cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), s);
-    const int mine = st == GESPMM_OK ? 0 : static_cast<int>(st);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(flag, &mine, sizeof(int), cudaMemcpyHostToDevice, s);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(flag, words, sizeof(int), cudaMemcpyHostToDevice, s);
     if (ce != cudaSuccess) return done(gespmm::cuda_fail(ce, "status agreement"));
     r = n.AllReduce(flag, flag, 1, kNcclInt32, kNcclMax, comm, s);
-    int agreed = 0;
-    if (r == 0) ce = cudaMemcpyAsync(&agreed, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (r == 0) ce = cudaMemcpyAsync(words + 1, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(flag, s);
     if (r != 0) return done(nccl_fail(r, "ncclAllReduce(status)"));
     const gespmm_status_t w = gespmm_comm_wait(comm, stream, o.timeout_ms > 0 ? o.timeout_ms : default_timeout_ms());
-    if (w != GESPMM_OK) return done(w);
+    if (w != GESPMM_OK) {
+      if (!plan) p = nullptr;  // the stream may never drain: do not synchronize on it
+      return w;
+    }
     if (ce != cudaSuccess) return done(gespmm::cuda_fail(ce, "status agreement"));
+    const int agreed = words[1];
     if (st != GESPMM_OK) return done(gespmm::fail(st, local_err));
     if (agreed != 0)
       return done(gespmm::fail(static_cast<gespmm_status_t>(agreed),
