@@ -633,11 +633,13 @@ def sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3000, seed=0, tag
 
 
 @pytest.mark.parametrize("workload,N", [("config2", 64), ("config4", 64), ("config4", 128), ("config4", 256),
-                                        ("config5", 128), ("config3", 256)])
+                                        ("config5", 128), ("config3", 16), ("config3", 32), ("config3", 64),
+                                        ("config3", 128), ("config3", 256)])
 def test_full_size_configs_sampled_bit_exact(cuda, oracle_mod, workload, N):
     """BASELINE configs 2-5 at full size (R-MAT scale 20/16M with N=64, scale
     22/64M with N=64/128/256, scale 24/2^30 edges with N=128, Reddit-like
-    114.6M nnz with N=256 in column panels) on one GPU: every op bit-exact to
+    114.6M nnz over config 3's whole N sweep 16-256: the paired-lane kernel,
+    the 16-gather fast batch, column panels) on one GPU: every op bit-exact to
     the twin AND within the north-star bound of the fp64 reference (max/min
     exact) on sampled rows incl. the 16 longest rows (up to ~10^5 nonzeros)."""
     import torch
