@@ -134,6 +134,10 @@ gespmm_status_t gespmm_comm_init(void** comm, int world, const char id[128], int
   nccl_comm_t c = nullptr;
   nccl_result_t r = n.CommInitRank(&c, world, u, rank);
   if (r != 0) return nccl_fail(r, "ncclCommInitRank");
+  {  // a new communicator may reuse the address of an aborted (freed) one
+    std::lock_guard<std::mutex> l(g_aborted_mu);
+    g_aborted.erase(c);
+  }
   *comm = c;
   return GESPMM_OK;
 }
