@@ -916,6 +916,25 @@ def test_comm_wait_timeout_aborts_instead_of_hanging(cuda):
     assert L.gespmm_comm_destroy(comm) == 0
 
 
+@pytest.mark.parametrize("args", [("20000", "5000", "128", "24", "4"), ("30000", "7000", "80", "16", "3"),
+                                  ("5000", "3000", "32", "8", "1")])
+def test_cpp_host_sharded_path(cuda, args):
+    """examples/sharded_host: a plain C++ host (no Python in the process) runs
+    the multi-GPU path through the C-ABI -- one NCCL rank per visible GPU,
+    per-rank validation + agreement, column-panelled B broadcast overlapped
+    with the compute, C all-gather, bounded wait -- and checks rank 0's full
+    C against a host fp64 sum under the north-star bound."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "sharded_host")
+    if not os.path.exists(exe):
+        pytest.skip("examples/sharded_host not built")
+    r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sharded_host ok" in r.stdout, r.stdout
+
+
 @pytest.mark.parametrize("op", OPS)
 def test_64bit_b_offsets(cuda, oracle_mod, op):
     """K * ldb > 2^32: the kernel's 64-bit B-row addressing path (staged 32-bit
