@@ -258,6 +258,51 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
       : "memory");
 #endif
 }
+// GESPMM_PIN=1: per-warp constants (the stage and ring shared addresses, the
+// lane's B base) are pinned in registers; ptxas otherwise recomputes them
+// from special registers and constants in every batch (config 5 ring: 85 ->
+// 68 SASS instructions per batch of 4 nonzeros; config 2: ~19 of ~60 per
+// batch of 8).
+#ifndef GESPMM_PIN
+#define GESPMM_PIN 1
+#endif
+// A value the compiler must keep in a register (an opaque move: it cannot be
+// rematerialized from the special registers / constants it came from).
+__device__ __forceinline__ uint32_t pin_reg(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+template <typename T>
+__device__ __forceinline__ T* pin_reg64(T* p) {
+  uint64_t y;
+  asm volatile("mov.b64 %0, %1;" : "=l"(y) : "l"(reinterpret_cast<uint64_t>(p)));
+  return reinterpret_cast<T*>(y);
+}
+// The same copy to a 32-bit shared-window address (the ring).
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const float* base, uint32_t off, uint64_t pol) {
+  (void)pol;
+  asm volatile(
+      "{\n .reg .u64 a;\n mad.wide.u32 a, %1, 4, %2;\n"
+      " cp.async.cg.shared.global [%0], [a], 16;\n}" ::"r"(dst),
+      "r"(off), "l"(base)
+      : "memory");
+}
+// VEC fp32 from a 32-bit shared-window address
+template <int VEC>
+__device__ __forceinline__ void lds_vec(float* d, uint32_t a);
+template <>
+__device__ __forceinline__ void lds_vec<1>(float* d, uint32_t a) {
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(d[0]) : "r"(a));
+}
+template <>
+__device__ __forceinline__ void lds_vec<2>(float* d, uint32_t a) {
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d[0]), "=f"(d[1]) : "r"(a));
+}
+template <>
+__device__ __forceinline__ void lds_vec<4>(float* d, uint32_t a) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]) : "r"(a));
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
@@ -373,7 +418,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   for (int w = 0; w < CWM; ++w) {
     cok[w] = colbase + w * TW < P.N;
     woff[w] = cok[w] ? static_cast<int>(colbase + w * TW) : 0;
-    bw[w] = P.B + woff[w];
+    bw[w] = GESPMM_PIN ? pin_reg64(P.B + woff[w]) : P.B + woff[w];
   }
   const int64_t ldb = P.ldb;
   // ring: this lane copies 16-byte chunk (lane % kLanesPerRow) of row
@@ -383,13 +428,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   float4* const ring = ring_smem + warp * (RING ? RG::kWarpBytes / 16 : 0);
   const int rchunk = lane % RG::kLanesPerRow;
   const int rsub = RG::kLanesPerRow >= 32 ? 0 : lane / RG::kLanesPerRow;
-  const float* const rsrc = [&] {
+  // the ring's 32-bit shared-window address, and B + this lane's column
+  // inside a B row: each copy is then rsrc + 4*offset (one LEA pair)
+  // (pinned in registers: ptxas otherwise recomputes them from special
+  // registers and constants in every batch -- 6-12 instructions per batch)
+  const uint32_t ring_s = RING ? pin_reg(static_cast<uint32_t>(__cvta_generic_to_shared(ring))) : 0u;
+  const float* const rsrc = pin_reg64(P.B + [&] {
     const int64_t c = static_cast<int64_t>(cb) * TW + 4 * rchunk;
-    return P.B + (c < P.N ? c : 0);
-  }();
+    return c < P.N ? c : 0;
+  }());
 #if GESPMM_SADDR
   int* const sc = stg[warp];
   float* const sv = reinterpret_cast<float*>(stg[warp] + kStageCap);
+  // the stage's 32-bit shared-window address (pinned: see pin_reg)
+  const uint32_t sc_s = GESPMM_PIN ? pin_reg(static_cast<uint32_t>(__cvta_generic_to_shared(sc)))
+                                   : static_cast<uint32_t>(__cvta_generic_to_shared(sc));
 #else
   int* const sc = scol[warp];
   float* const sv = sval[warp];
@@ -642,7 +695,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
 #if GESPMM_SADDR
     // 32-bit shared address of stage entry 0 relative to position 0
-    const uint32_t s_pos0 = static_cast<uint32_t>(__cvta_generic_to_shared(sc)) - 4u * static_cast<uint32_t>(sbase);
+    const uint32_t s_pos0 = sc_s - 4u * static_cast<uint32_t>(sbase);
 #endif
     // the 4 staged offsets / values at positions qb + 4g .. qb + 4g + 3
     auto stage_off4 = [&](int qb, int g) {
@@ -669,7 +722,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     };
     // ring: copy batch qb into slot, one commit group per batch
     auto issue_ring = [&](int qb, int slot) {
-      float4* dst = ring + slot * (U * RG::kLanesPerRow);
+      const uint32_t dst = ring_s + static_cast<uint32_t>((slot * U + rsub) * RG::kRowBytes + rchunk * 16);
       // the batch's offsets with 128-bit broadcast loads (no per-row LDS
       // latency chain); each lane then picks the row it copies
       int offs[U];
@@ -684,7 +737,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         int off = offs[g];
 #pragma unroll
         for (int r = 1; r < RG::kRowsPerIssue; ++r) off = rsub == r ? offs[g + r] : off;
-        cp_async16_b(dst + (g + rsub) * RG::kLanesPerRow + rchunk, rsrc, static_cast<uint32_t>(off), pol);
+        cp_async16_s(dst + g * RG::kRowBytes, rsrc, static_cast<uint32_t>(off), pol);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -699,8 +752,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       }
     };
     auto ring_row = [&](int slot, int u, float (&d)[CWM][VEC]) {
-      const float* r = reinterpret_cast<const float*>(ring + (slot * U + u) * RG::kLanesPerRow);
-      Vec<VEC>::ld(d[0], r + lane * VEC);
+      lds_vec<VEC>(d[0], ring_s + static_cast<uint32_t>((slot * U + u) * RG::kRowBytes + lane * VEC * 4));
     };
     auto consume = [&](int qb, const float (&b)[U][CWM][VEC]) {
       float v[U];
