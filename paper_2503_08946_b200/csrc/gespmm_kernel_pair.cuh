@@ -51,10 +51,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
   const int64_t colbase = static_cast<int64_t>(cb) * TW + gl * VEC;
   const bool cok = colbase < P.N;
   const int woff = cok ? static_cast<int>(colbase) : 0;
-  const float* bw = P.B + woff;
+  const float* bw = GESPMM_PIN ? pin_reg64(P.B + woff) : P.B + woff;  // pinned: see pin_reg
   const int64_t ldb = P.ldb;
   const int64_t ldc = P.ldc;
   int* const sc = stg[warp];
+  const uint32_t sc_s = GESPMM_PIN ? pin_reg(static_cast<uint32_t>(__cvta_generic_to_shared(sc)))
+                                   : static_cast<uint32_t>(__cvta_generic_to_shared(sc));
   float* const sv = reinterpret_cast<float*>(stg[warp] + kStageCap);
   int* const rp = rpw[warp];
   const bool accumulate = P.accumulate != 0;
@@ -251,8 +253,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     else row_seed(lo, crow);
 
     // 32-bit shared address of my half's entries of position-block 0
-    const uint32_t s_pos0 = static_cast<uint32_t>(__cvta_generic_to_shared(sc)) +
-                            4u * static_cast<uint32_t>(H * g - sbase);
+    const uint32_t s_pos0 = sc_s + 4u * static_cast<uint32_t>(H * g - sbase);
     for (int qb = sbase; qb < hi; qb += U) {
       // my half's four staged entries of this batch: positions qb + 2i + g
       float b[H][VEC];
