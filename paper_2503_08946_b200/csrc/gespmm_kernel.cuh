@@ -426,6 +426,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     woff[w] = cok[w] ? woff[w] : 0;
     bw[w] = GESPMM_PIN ? pin_reg64(P.B + woff[w]) : P.B + woff[w];
   }
+  // every lane of this column block has real columns (warp-uniform): the
+  // per-lane guard (rematerialized by ptxas at every row end) is then skipped
+  // -- config 2 sum / max 0.338 / 0.343 -> 0.334 / 0.338 ms; not at one column
+  // per lane, where it cost config 3 N=32 1.151 -> 1.171 ms (profiles/r2_pin/)
+  const bool all_ok = static_cast<int64_t>(cb + 1) * (TW * CWM) <= P.N;
   const int64_t ldb = P.ldb;
   // ring: this lane copies 16-byte chunk (lane % kLanesPerRow) of row
   // (lane / kLanesPerRow) of every kRowsPerIssue-row group; a chunk past N
@@ -488,7 +493,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     if (GESPMM_ABL_NOSTORE) return;  // ablation builds only
 #pragma unroll
     for (int w = 0; w < CWM; ++w) {
-      if (!cok[w]) continue;
+      if (!((CPL >= 2 && all_ok) || cok[w])) continue;
       float o[VEC];
       float c0[VEC];
       if (!SR::kSeedC0 && accumulate) Vec<VEC>::ld(c0, dst + (woff[w] - woff[0]));
