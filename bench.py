@@ -12,7 +12,8 @@ GPU at N=1 and row-sharded (strong scaling) at N>1.  Synthetic, seeded,
 generated on the GPU with torch ops (workloads.rmat_csr) -- the SAME generator
 and seed in both arms, so the reference arm reads the identical matrix
 (``input`` carries a fingerprint in both lines).  configs[1] (R-MAT scale 20,
-N=64) rides along at N=1 under ``extra`` (kernel, roofline, e2e).
+N=64) and configs[3] (R-MAT scale 22, N=128) ride along at N=1 under
+``extra`` (kernel, roofline, e2e, each with its own clock record).
 
 A step = one execution of the hot path over the matrix with a cached plan
 (one kernel launch per column panel, after a reset of its item counter).
@@ -64,7 +65,7 @@ def parse_args(argv=None):
     ap.add_argument("--workload", default="config5")
     ap.add_argument("--op", default="sum", choices=["sum", "max", "min", "mean"])
     ap.add_argument("--N", type=int, default=0, help="override the workload's dense width (sweeps)")
-    ap.add_argument("--extra", default="config2",
+    ap.add_argument("--extra", default="config2,config4",
                     help="N=1: comma-separated workloads measured after the headline one (kernel, roofline, "
                          "e2e) and reported under 'extra'; '' = none")
     ap.add_argument("--generator", default="torch", choices=["torch", "native"],
@@ -796,14 +797,20 @@ def measure_extra(args, name, dev):
     """A secondary workload at N=1: kernel steps, roofline, gather ceiling, e2e."""
     import torch
 
+    from paper_2503_08946_b200.spmm import variant_name
+
     m = Measure(args, name, dev, 1, 0, 0)
+    nvml = NvmlSampler(dev.index or 0, enabled=not args.no_clocks)
+    nvml.start()
     times = m.steps(args.steps, args.warmup)
+    clk = nvml.stop("warm-up + timed steps")
     t = sum(times) / len(times)
     flops = 2.0 * m.nnz_all * m.N
     out = {"workload": m.spec["desc"], "op": args.op, "N": m.N, "nnz": m.nnz_all, "input": m.fp,
            "value": flops / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
            "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
-           "roofline": m.roofline(t), "gather_ceiling": m.gather_ceiling(t)}
+           "roofline": m.roofline(t), "gather_ceiling": m.gather_ceiling(t), "clocks": clk,
+           "kernel_variant": variant_name(m.N, m.B, m.C, args.op)}
     if not args.no_e2e:
         out["e2e"] = m.e2e_single(flops, reps=max(3, min(args.steps, 10)))
     del m

@@ -48,7 +48,7 @@ def test_defaults_are_the_north_star_run():
     column-panelled B broadcast; configs[1] rides along at N=1."""
     a = bench.parse_args([])
     assert a.workload == "config5" and a.scaling == "strong" and a.gpus == 1
-    assert a.extra == "config2" and a.generator == "torch" and a.b_panels > 1
+    assert a.extra == "config2,config4" and a.generator == "torch" and a.b_panels > 1
     assert a.warmup >= 3
 
 

@@ -40,6 +40,7 @@ def test_bench_line_contract():
     assert e["equals_device_result"] is True
     x = d["extra"]["config1"]
     assert "error" not in x, x
+    assert x["clocks"] is None or x["clocks"]["sm_max_mhz"] > 0
     assert x["value"] > 0 and x["e2e"]["value"] > 0 and x["e2e"]["equals_device_result"] is True
 
 
