@@ -5,6 +5,8 @@ reference; and -- stronger -- bit-identical to the fp32 twin
 (oracle/gespmm_oracle.c) for every op, every kernel variant, split and
 unsplit rows.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -581,6 +583,36 @@ def test_config2_full_size_bit_exact(cuda, oracle_mod, op):
     want = oracle_mod.spmm_f32(csr.rowptr.cpu().numpy(), csr.colind.cpu().numpy(),
                                csr.vals.cpu().numpy(), B.cpu().numpy(), op, seg_len=SEG)
     np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("workload,op", [("config4", "sum"), ("config4", "mean"), ("config5", "sum"),
+                                         ("config3-256", "sum")])
+def test_full_size_whole_matrix_bit_exact(cuda, oracle_mod, workload, op):
+    """Every cell, not a sample: the headline configuration (config 5: R-MAT
+    2^24, 1.02 B nonzeros, N=128 -- 2.1 G output cells), config 4 and config 3
+    at N=256 (column panels), exactly as bench.py generates them, against the
+    fp32 twin on all host cores (~30 GB of host memory for config 5)."""
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2503_08946_b200.spmm import Plan
+
+    spec = bench.workload_spec(workload)
+    csr, B = bench.make_workload(spec, cuda, "torch")
+    plan = Plan(csr.rowptr, csr.colind, csr.K)
+    got = plan.execute(csr.vals, B, op)
+    torch.cuda.synchronize()
+    got_h = got.cpu().numpy()
+    del got
+    args = [t.cpu().numpy() for t in (csr.rowptr, csr.colind, csr.vals, B)]
+    del csr, B, plan
+    torch.cuda.empty_cache()
+    want = oracle_mod.spmm_f32(*args, op, seg_len=SEG)
+    neq = int(np.count_nonzero(got_h.view(np.uint32) != want.view(np.uint32)))
+    assert neq == 0, f"{workload} {op}: {neq} of {want.size} cells differ from the twin"
 
 
 def sampled_rows_bit_exact(oracle_mod, csr, B, C, op, n_random=3000, seed=0, tag=""):
