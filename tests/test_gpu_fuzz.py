@@ -1,7 +1,8 @@
 """Randomized parity sweep (seeded, deterministic): shapes, densities, long
 rows, empty rows, duplicate/unsorted columns, odd N, strided/misaligned B and
 C, accumulate, every reduce op, both item schedules, forced column panels and
-forced kernel variants -- GPU bit-exact to the fp32 twin in every case."""
+forced kernel variants, the cached-plan and the one-shot entry points -- GPU
+bit-exact to the fp32 twin in every case."""
 import os
 
 import numpy as np
@@ -73,9 +74,15 @@ def test_fuzz_bit_exact(cuda, oracle_mod, case):
     spmm.set_panel_override(int(rng.choice([-1, -1, 0, 32, 64])))
     tw = int(rng.choice([0, 0, 2, 13, 32, 256]))
     spmm.set_tile_work_override(tw)
+    # every third case through the one-shot entry point (gespmm_csr_spmm: the
+    # plan built on the device with a-priori item bounds, one trailing sync)
+    oneshot = case % 3 == 2
     try:
-        plan = Plan(rp, ci, K)
-        plan.execute(vv, Bt, op, out=Ct, accumulate=accumulate)
+        if oneshot:
+            spmm.csr_spmm(rp, ci, vv, Bt, op, out=Ct, accumulate=accumulate)
+        else:
+            plan = Plan(rp, ci, K)
+            plan.execute(vv, Bt, op, out=Ct, accumulate=accumulate)
         torch.cuda.synchronize()
     finally:
         spmm.set_variant_override("")
@@ -84,7 +91,8 @@ def test_fuzz_bit_exact(cuda, oracle_mod, case):
         spmm.set_tile_work_override(0)
     want = oracle_mod.spmm_f32(rowptr, colind, vals, B, op, accumulate=accumulate, C0=C0, seg_len=SEG)
     got = Ct.cpu().numpy()
-    np.testing.assert_array_equal(got, want, err_msg=f"case {case}: M={M} K={K} N={N} op={op} variant={variant} tw={tw}")
+    np.testing.assert_array_equal(got, want, err_msg=f"case {case}: M={M} K={K} N={N} op={op} variant={variant} "
+                                                     f"tw={tw} oneshot={oneshot}")
     if op in ("max", "min"):  # maximumNumber: every bit, NaNs included
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=f"case {case} bits")
     # nothing outside the C view was written
