@@ -32,7 +32,7 @@
 //    registers), then folded; at one column per lane (N <= 32 tiles) runs of
 //    16 in-row positions are gathered at once.  The memory-level parallelism
 //    this buffer allows is the kernel's bound (tools/gather_probe.cu: the
-//    gather-only replay of the same stream at the same MLP takes ~88 % of
+//    gather-only replay of the same stream at the same MLP takes ~90 % of
 //    the kernel's time).  TMA gather4 reaches only 3-7 TB/s for 256-byte rows,
 //    so the gathers stay in LDG.  At 512-byte rows (N=128 tiles) the B rows
 //    instead go through a per-warp shared-memory ring with cp.async (Ring<>),
