@@ -36,12 +36,12 @@ constexpr int kWarpsPerBlock = 8;
 // staging starts at the 16-byte-aligned position below the item start.
 // 576: 8 warps x 576 x 8 B = 36.9 KB per CTA, so three CTAs fit per SM next
 // to the gather ring (8 x 4 KB); the bound below covers the 4-alignment of the
-// stage start and the rounding of its end up to a batch of 8.
+// stage start and the rounding of its end up to a batch of (at most) 12.
 #ifndef GESPMM_STAGE_CAP
 #define GESPMM_STAGE_CAP 576
 #endif
 constexpr int kStageCap = GESPMM_STAGE_CAP;
-static_assert(kTileWork + kSeg + kRowCost + 2 + 3 + 8 <= kStageCap, "stage too small for the largest item");
+static_assert(kTileWork + kSeg + kRowCost + 2 + 3 + 12 <= kStageCap, "stage too small for the largest item");
 // Low 40 bits of the packed plan scan carry tile work, high 24 bits segment counts.
 constexpr int kPackShift = 40;
 // Column panels: B slabs larger than this are processed in column panels

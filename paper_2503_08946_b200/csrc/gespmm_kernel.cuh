@@ -28,8 +28,8 @@
 //    of CWM column tiles, so one staged (col, val) pair feeds VEC*CWM FMAs and
 //    every B-row gather is one fully coalesced 32*VEC*4-byte warp access.
 //  * Gather pipeline: B-row gathers are issued in batches of U = 8 nonzeros
-//    into one register buffer (16 registers at N=64; 32 warps/SM at 64
-//    registers), then folded; at one column per lane (N <= 32 tiles) runs of
+//    (12 for sum at N=64) into one register buffer (16-24 registers at N=64;
+//    32 warps/SM at 64 registers), then folded; at one column per lane (N <= 32 tiles) runs of
 //    16 in-row positions are gathered at once.  The memory-level parallelism
 //    this buffer allows is the kernel's bound (tools/gather_probe.cu: the
 //    gather-only replay of the same stream at the same MLP takes ~90 % of
@@ -332,9 +332,16 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #if (GESPMM_ABL_NOSTORE || GESPMM_ABL_NOGATHER) && !defined(GESPMM_EXPERIMENT_BUILD)
 #error "GESPMM_ABL_NOSTORE/NOGATHER give wrong results: tagged experiment builds only (GESPMM_BUILD_TAG)"
 #endif
-template <int CPL>
+// sum at two columns per lane (the 64-column tile) runs 12-row batches: 50 %
+// more rows in flight for a 24-byte spill outside the batch loop -- config 4 /
+// 5 at N=64 1.467 -> 1.416 / 26.3 -> 25.7 ms, config 2 0.335 -> 0.332 ms;
+// max lost (0.338 -> 0.343 ms), so the other ops keep 8 (profiles/r2_pin/r2_c30_*)
+#ifndef GESPMM_U_SUM2
+#define GESPMM_U_SUM2 12
+#endif
+template <int CPL, gespmm_reduce_t OP>
 struct Pipe {
-  static constexpr int U = CPL >= 4 ? 4 : GESPMM_U_NARROW;
+  static constexpr int U = CPL >= 4 ? 4 : (CPL == 2 && OP == GESPMM_REDUCE_SUM) ? GESPMM_U_SUM2 : GESPMM_U_NARROW;
 };
 
 #ifndef GESPMM_MINBLOCKS
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   // even chain).  max/min: one chain in slot 0.
   constexpr bool TWO = SR::kFma2;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
-  constexpr int U = RING ? Ring<VEC, CWM>::U : Pipe<CPL>::U;  // gathers per batch
+  constexpr int U = RING ? Ring<VEC, CWM>::U : Pipe<CPL, OP>::U;  // gathers per batch
   constexpr int FB = RING ? 0 : CPL == 1 ? GESPMM_FAST_VEC1 : CPL == 2 ? GESPMM_FAST_VEC2 : 0;  // in-row fast batch
   using RG = Ring<VEC, CWM>;
   static_assert(!RING || RG::kSupported, "ring mode: CWM == 1, VEC >= 2");
