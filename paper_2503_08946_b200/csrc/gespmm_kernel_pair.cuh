@@ -216,31 +216,41 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     if (lane < lo - sbase) sc[lane] = 0;  // head: another item's entries, never gathered through
     __syncwarp();
     {
+      // per 8-entry block: the 4 even positions, then the 4 odd ones (a half's
+      // 4 entries of the block contiguous).  Lane l holds entries 4l..4l+3
+      // (coalesced 128-bit loads and stores, no bank conflicts); lane pairs
+      // (2m, 2m+1) own block m and swap one entry pair with shfl_xor(1): the
+      // even lane keeps its evens and takes its partner's, the odd lane the
+      // odds.  (A lane-per-block permutation reads and writes at a 64-byte
+      // lane stride: 16-way bank conflicts, ~25 % of the L1 data-pipe
+      // wavefronts at config 3 N=16.)  The trip count is warp-uniform for the
+      // shuffles; the span is a multiple of U >= 8, so a pair is in or out
+      // together.
       const uint32_t ldb32 = static_cast<uint32_t>(ldb);
-      // per U-block: even offsets first, then odd (a half's entries contiguous);
-      // lane l permutes block l (U <= 16 entries: held in registers)
-      for (int i = U * lane; i < send - sbase; i += 32 * U) {
-        int c[U];
-        float w[U];
-#pragma unroll
-        for (int q = 0; q < U; q += 4) {
-          const int4 a = *reinterpret_cast<int4*>(sc + i + q);
-          const float4 f = *reinterpret_cast<float4*>(sv + i + q);
-          c[q] = a.x, c[q + 1] = a.y, c[q + 2] = a.z, c[q + 3] = a.w;
-          w[q] = f.x, w[q + 1] = f.y, w[q + 2] = f.z, w[q + 3] = f.w;
+      const bool odd = lane & 1;
+      const int len = send - sbase;
+      for (int i0 = 0; i0 < len; i0 += 128) {
+        const int i = i0 + 4 * lane;
+        const bool in = i < len;
+        int4 a = make_int4(0, 0, 0, 0);
+        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in) {
+          a = *reinterpret_cast<int4*>(sc + i);
+          f = *reinterpret_cast<float4*>(sv + i);
         }
+        const int ra = __shfl_xor_sync(FULL, odd ? a.x : a.y, 1);
+        const int rb = __shfl_xor_sync(FULL, odd ? a.z : a.w, 1);
+        const float ga = __shfl_xor_sync(FULL, odd ? f.x : f.y, 1);
+        const float gb = __shfl_xor_sync(FULL, odd ? f.z : f.w, 1);
+        int d[4] = {odd ? ra : a.x, odd ? rb : a.z, odd ? a.y : ra, odd ? a.w : rb};
+        const float x[4] = {odd ? ga : f.x, odd ? gb : f.z, odd ? f.y : ga, odd ? f.w : gb};
+        if (OFF32) {
 #pragma unroll
-        for (int q = 0; q < U; q += 4) {
-          int d[4];
-          float x[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int src = ((q + r) < H) ? 2 * (q + r) : 2 * (q + r - H) + 1;
-            d[r] = OFF32 ? static_cast<int>(static_cast<uint32_t>(c[src]) * ldb32) : c[src];
-            x[r] = w[src];
-          }
-          *reinterpret_cast<int4*>(sc + i + q) = make_int4(d[0], d[1], d[2], d[3]);
-          *reinterpret_cast<float4*>(sv + i + q) = make_float4(x[0], x[1], x[2], x[3]);
+          for (int r = 0; r < 4; ++r) d[r] = static_cast<int>(static_cast<uint32_t>(d[r]) * ldb32);
+        }
+        if (in) {
+          *reinterpret_cast<int4*>(sc + i) = make_int4(d[0], d[1], d[2], d[3]);
+          *reinterpret_cast<float4*>(sv + i) = make_float4(x[0], x[1], x[2], x[3]);
         }
       }
       __syncwarp();
@@ -252,10 +262,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     if (!is_tile && it.y > 0) seed(lo, SR::identity(), nullptr);
     else row_seed(lo, crow);
 
-    // 32-bit shared address of my half's entries of position-block 0
-    const uint32_t s_pos0 = sc_s + 4u * static_cast<uint32_t>(H * g - sbase);
+    // 32-bit shared address of my half's entries of 8-entry block 0
+    const uint32_t s_pos0 = sc_s + 4u * static_cast<uint32_t>(4 * g - sbase);
     for (int qb = sbase; qb < hi; qb += U) {
-      // my half's four staged entries of this batch: positions qb + 2i + g
+      // my half's staged entries of this batch, four per 8-entry block:
+      // entry i is position qb + 2i + g
       float b[H][VEC];
       float v[H];
 #pragma unroll
@@ -263,7 +274,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
         int4 o;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
-                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + 16u * q4));
+                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + 32u * q4));
         gather(b[4 * q4 + 0], o.x);
         gather(b[4 * q4 + 1], o.y);
         gather(b[4 * q4 + 2], o.z);
@@ -274,7 +285,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
         float4 vv;
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(vv.x), "=f"(vv.y), "=f"(vv.z), "=f"(vv.w)
-                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + (4u * kStageCap + 16u * q4)));
+                     : "r"(s_pos0 + 4u * static_cast<uint32_t>(qb) + (4u * kStageCap + 32u * q4)));
         v[4 * q4] = vv.x, v[4 * q4 + 1] = vv.y, v[4 * q4 + 2] = vv.z, v[4 * q4 + 3] = vv.w;
       }
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: the batch is in the current row

@@ -52,7 +52,7 @@ bool parse_variant(const char* name, Variant* v) {
 // Tile shape selected by N and op (north star item (1)): fewest idle lanes,
 // then fewest column blocks, then the table order above.
 Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, int64_t ldc,
-                       gespmm_reduce_t /*op: every variant implements every op*/) {
+                       gespmm_reduce_t op /* every variant implements every op */) {
   auto aligned = [&](int vec) {
     const uintptr_t a = static_cast<uintptr_t>(vec) * 4;
     return reinterpret_cast<uintptr_t>(B) % a == 0 && reinterpret_cast<uintptr_t>(C) % a == 0 &&
@@ -60,6 +60,16 @@ Variant choose_variant(int64_t N, const float* B, int64_t ldb, const float* C, i
   };
   Variant best{1, 1, false};
   int64_t best_idle = -1, best_ncb = 0;
+  // max/min at the 32-column tile: the paired-lane kernel first (FMUL2 +
+  // FMNMX3 over two positions per warp instruction; config 3 N=32 max 1.286
+  // -> 1.218 ms); sum/mean keep the 32-lane kernel there (1.159 vs 1.186 ms,
+  // profiles/r2_pairperm/)
+  const bool pair_first = (op == GESPMM_REDUCE_MAX || op == GESPMM_REDUCE_MIN) && N > 16 && N <= 32;
+  if (pair_first && aligned(2)) {
+    best = Variant{2, 1, true, false};
+    best_idle = 32 - N;
+    best_ncb = 1;
+  }
   for (const Variant& c : kVariants) {
     if (!aligned(c.vec) || c.ring) continue;
     const int64_t cols = variant_cols(c);

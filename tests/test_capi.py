@@ -111,7 +111,10 @@ def test_variant_selection_by_N():
     assert variant_name(256) == "vec4_lpr32_cwm2"
     assert variant_name(512) == "vec4_lpr32_cwm2"
     assert variant_name(33) == "pair_vec1"  # 3 blocks of 16: 15 idle columns vs 31
-    assert variant_name(32, reduce="min") == "vec1_lpr32_cwm1"
+    # max/min at the 32-column tile: the paired-lane kernel (profiles/r2_pairperm/)
+    assert variant_name(32, reduce="min") == "pair_vec2"
+    assert variant_name(32, reduce="max") == "pair_vec2"
+    assert variant_name(32, reduce="mean") == "vec1_lpr32_cwm1"
     assert variant_name(64, reduce="max") == "vec2_lpr32_cwm1"
     assert variant_name(33, reduce="max") == "pair_vec1"
 
