@@ -30,13 +30,18 @@ namespace kern {
 #ifndef GESPMM_PAIR_U
 #define GESPMM_PAIR_U 16  // measured: config 3 N=16 1.356 -> 1.255 ms vs 8
 #endif
+#ifndef GESPMM_PAIR_U1
+#define GESPMM_PAIR_U1 GESPMM_PAIR_U  // one column per lane (N <= 16)
+#endif
 template <gespmm_reduce_t OP, int VEC, bool OFF32>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     spmm_pair_kernel(const KParams P) {
   using SR = Semiring<OP>;
   static_assert(SR::kFma2 || SR::kMnmx, "paired lanes: two-chain sum/mean or order-free max/min");
-  constexpr int U = GESPMM_PAIR_U;  // positions per batch (U/2 per half; 8 or 16)
+  constexpr int U = VEC == 1 ? GESPMM_PAIR_U1 : GESPMM_PAIR_U;  // positions per batch (U/2 per half; 8, 16 or 32)
   constexpr int H = U / 2;
+  static_assert(U % 8 == 0 && kTileWork + kSeg + kRowCost + 2 + 3 + U <= kStageCap,
+                "the stage holds the largest item rounded up to a batch");
   constexpr int TW = 16 * VEC;   // columns per column block
   constexpr unsigned FULL = 0xffffffffu;
   // per warp: colind slice then vals slice (vals at an immediate offset)
