@@ -559,13 +559,21 @@ class Measure:
         self.rowptr, self.colind, self.vals, self.B = rowptr, colind, vals, B
         self.M_loc, self.nnz_loc = rowptr.numel() - 1, colind.numel()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        e0.record(stream)
-        self.plan = Plan(rowptr, colind, K)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        self.plan_ms = e0.elapsed_time(e1)
-        self.plan_wall_ms = (time.perf_counter() - t0) * 1e3
+
+        def build_plan():
+            t0 = time.perf_counter()
+            e0.record(stream)
+            plan = Plan(rowptr, colind, K)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return plan, e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3
+
+        # the first plan of the process also pays one-time costs (lazy module
+        # loading of the plan kernels, the stream-ordered pool's first growth);
+        # the plan a repeated call builds is the second one
+        first, self.plan_first_ms, _ = build_plan()
+        first.close()
+        self.plan, self.plan_ms, self.plan_wall_ms = build_plan()
         self.info = self.plan.info()
         self.C = torch.empty((self.M_loc, N), dtype=torch.float32, device=dev)
         l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -924,7 +932,9 @@ def main():
                                        else "single GPU"),
                        "plan": {"n_items": info["n_items"], "n_long_rows": info["n_long_rows"],
                                 "n_segments": info["n_segments"], "build_ms": m.plan_ms,
-                                "build_wall_ms": m.plan_wall_ms},
+                                "build_wall_ms": m.plan_wall_ms, "first_build_ms": m.plan_first_ms,
+                                "what": "device time of a fresh plan (the process's second; the first "
+                                        "also pays one-time module loading and pool growth)"},
                        "b_broadcast_ms": m.bcast_ms},
             "hbm_gbs_algorithmic": roof["achieved"],
             "roofline": roof,
