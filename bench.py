@@ -818,7 +818,7 @@ def measure_extra(args, name, dev):
            "value": flops / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
            "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
            "roofline": m.roofline(t), "gather_ceiling": m.gather_ceiling(t), "clocks": clk,
-           "kernel_variant": variant_name(m.N, m.B, m.C, args.op)}
+           "kernel_variant": m.plan.last_variant() or variant_name(m.N, m.B, m.C, args.op)}
     if not args.no_e2e:
         out["e2e"] = m.e2e_single(flops, reps=max(3, min(args.steps, 10)))
     del m
@@ -946,7 +946,7 @@ def main():
             "c_allgather": c_allgather,
             "gpu_launches": args.steps * int(info["kernel_launches_per_execute"]) * n_panels,
             "panel_cols": pw,
-            "kernel_variant": variant_name(N, m.B, m.C, args.op),
+            "kernel_variant": m.plan.last_variant() or variant_name(N, m.B, m.C, args.op),
             "step_ms": {"min": min(times), "median": statistics.median(times), "max": max(times)},
         }
     del m

@@ -587,13 +587,15 @@ __global__ void __launch_bounds__(256, 1) probe_tma(const __grid_constant__ CUte
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int RB = 512, STAGE = G * 4 * RB;
   __shared__ __align__(8) uint64_t bar[8][S];
+  __shared__ __align__(16) int scratch[8][4 * G];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* ring = smraw + wib * S * STAGE;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  uint64_t pl, pf;
+  uint64_t pl, pf, pn;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pn));
   if (lane < S) {
     const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][lane]));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
@@ -607,7 +609,7 @@ __global__ void __launch_bounds__(256, 1) probe_tma(const __grid_constant__ CUte
     const int64_t s1 = s0 + span < nidx ? s0 + span : nidx;
     const int nb = static_cast<int>((s1 - s0) / PER);  // whole stages only (the tail is skipped: a probe)
     auto issue = [&](int k) {
-      if (k >= nb || lane != 0) return;
+      if (MODE >= 2 || k >= nb || lane != 0) return;  // grouped modes: issue_grouped
       const int d = k % S;
       const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(STAGE) : "memory");
@@ -634,9 +636,51 @@ __global__ void __launch_bounds__(256, 1) probe_tma(const __grid_constant__ CUte
         }
       }
     };
+    // window grouping (what a kernel can do): the stage's PER positions
+    // regrouped hot-first into its gather4s -- lanes < PER each take one
+    // position, a ballot gives each its slot, the row indices go through a
+    // per-warp scratch to the issuing lane; the consumer would read slot
+    // sigma(u) for position u.  All-hot group: evict_last; all-cold:
+    // evict_first; mixed: evict_first (MODE 2) / evict_normal (MODE 3).
+    auto issue_grouped = [&](int k) {
+      if (k >= nb) return;
+      const int d = k % S;
+      const int* ip = idx + s0 + static_cast<int64_t>(k) * PER;
+      const int e = lane < PER ? __ldg(ip + lane) : 0;
+      const unsigned hm = __ballot_sync(0xffffffffu, lane < PER && e < 0);
+      const int nh = __popc(hm);
+      const unsigned lt = (1u << lane) - 1u;
+      const int slot = (e < 0) ? __popc(hm & lt) : nh + __popc(~hm & lt & ((1u << PER) - 1u));
+      if (lane < PER) scratch[wib][slot] = e & 0x7fffffff;
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(STAGE) : "memory");
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int4 rr = *reinterpret_cast<const int4*>(&scratch[wib][4 * g]);
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(ring + d * STAGE + g * 4 * RB));
+          const int hot_in = min(max(nh - 4 * g, 0), 4);
+          // MODE 4: the grouping alone (every group evict_normal) -- its cost
+          const uint64_t pol =
+              MODE == 4 ? pn : hot_in == 4 ? pl : hot_in == 0 ? pf : (MODE == 2 ? pf : pn);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+              "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(rr.x), "r"(rr.y), "r"(rr.z), "r"(rr.w), "r"(b),
+              "l"(pol)
+              : "memory");
+        }
+      }
+      __syncwarp();
+    };
+    if (MODE >= 2) {
+      for (int k = 0; k < S - 1; ++k) issue_grouped(k);
+    }
     for (int k = 0; k < S - 1; ++k) issue(k);
     for (int k = 0; k < nb; ++k) {
-      issue(k + S - 1);
+      if (MODE >= 2) issue_grouped(k + S - 1);
+      else issue(k + S - 1);
       const int d = k % S;
       const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[wib][d]));
       const uint32_t par = (phase >> d) & 1u;
@@ -683,12 +727,20 @@ extern "C" float l2hot_probe_tma(const float* B, int64_t K, const int* idx, int6
   else if (S == 3 && G == 2) { X(3, 2) }             \
   else if (S == 2 && G == 2) { X(2, 2) }             \
   else if (S == 6 && G == 1) { X(6, 1) }             \
+  else if (S == 2 && G == 4) { X(2, 4) }             \
+  else if (S == 3 && G == 4) { X(3, 4) }             \
   else return -2.f;
 #define TMA_SET(a, b)                                                                                        \
   cudaFuncSetAttribute(probe_tma<a, b, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);              \
-  cudaFuncSetAttribute(probe_tma<a, b, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(probe_tma<a, b, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);              \
+  cudaFuncSetAttribute(probe_tma<a, b, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);              \
+  cudaFuncSetAttribute(probe_tma<a, b, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);              \
+  cudaFuncSetAttribute(probe_tma<a, b, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 #define TMA_RUN(a, b)                                                                              \
   if (mode == 1) probe_tma<a, b, 1><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);              \
+  else if (mode == 2) probe_tma<a, b, 2><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);         \
+  else if (mode == 3) probe_tma<a, b, 3><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);         \
+  else if (mode == 4) probe_tma<a, b, 4><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);         \
   else probe_tma<a, b, 0><<<grid, 256, smem>>>(tm, idx, nidx, span, sink);
   TMA_ALL(TMA_SET)
   cudaEvent_t e0, e1;

@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--bulk", default="", help="bulk-copy ring configs vec:U:D;... e.g. 2:16:2,4:8:4")
     ap.add_argument("--pinned", default="", help="pinned hot set + plain LDGSTS ring, configs U:D:warps_per_sm")
     ap.add_argument("--tma", default="", help="TMA gather4 ring configs S:G:warps_per_sm, e.g. 4:1:24,3:2:16")
+    ap.add_argument("--tma-mode", type=int, default=1,
+                    help="--tma with a hot set: 1 = per-gather4 hint (any hot row -> evict_last), 2 / 3 = the "
+                         "stage's positions regrouped hot-first, mixed groups evict_first / evict_normal")
     ap.add_argument("--tma-sorted", action="store_true",
                     help="--tma: within each span, hot positions first (stable) -- the best case for a "
                          "per-gather4 hint (gather order may differ from fold order)")
@@ -80,9 +83,11 @@ def main():
                 del perm
             for cfg in a.tma.split(","):
                 S_, G_, wps = (int(x) for x in cfg.split(":"))
-                ms = L.l2hot_probe_tma(B.data_ptr(), K, flagged.data_ptr(), col.numel(), 1 if mb else 0, S_, G_, wps,
+                ms = L.l2hot_probe_tma(B.data_ptr(), K, flagged.data_ptr(), col.numel(), a.tma_mode if mb else 0,
+                                       S_, G_, wps,
                                        a.span, a.reps, sink.data_ptr(), flush.data_ptr(), flush.numel())
-                print(json.dumps({"tma": cfg, "mode": 1 if mb else 0, "hot_mb": mb, "sorted": bool(a.tma_sorted),
+                print(json.dumps({"tma": cfg, "mode": a.tma_mode if mb else 0, "hot_mb": mb,
+                                  "sorted": bool(a.tma_sorted),
                                   "hot_share": round(float(cum[H - 1]), 4) if H else 0, "ms": round(ms, 3)}),
                       flush=True)
             del flagged
