@@ -225,15 +225,8 @@ gespmm_status_t gespmm_set_schedule_override(int mode);
  * in [2, 256].  Results are identical for every value (rows stay whole).
  * Test/tuning knob; not thread-safe. */
 gespmm_status_t gespmm_set_tile_work_override(int32_t units);
-/* The TMA gather4 ring with an L2 hot set (DESIGN.md 5.2 "TMA ring") for
- * the 128-column ring tile: mode -1 = automatic (when B's K x 128 slab exceeds
- * the L2 budget), 0 = off (the cp.async ring), 1 = wherever the ring tile runs.
- * hot_rows: the hot set's size in B rows (-1 = automatic, 80 MB of rows; 0 =
- * none).  Results are identical in every mode.  Test/tuning knob; not
- * thread-safe. */
-gespmm_status_t gespmm_set_tma_override(int mode, int64_t hot_rows);
 /* The kernel variant the plan's last execute launched (diagnostics; "" before
- * the first execute), e.g. "vec4_lpr32_cwm1_ring_tma". */
+ * the first execute), e.g. "vec4_lpr32_cwm1_ring". */
 const char* gespmm_plan_last_variant(gespmm_plan_t plan);
 /* The panel width gespmm_plan_execute uses for a K-row B with N columns: one
  * kernel launch per panel, ceil(N / width) launches per execute. */

@@ -29,7 +29,7 @@ EXPORTS = [
     "gespmm_rmat_csr", "gespmm_uniform_fill", "gespmm_coo_to_csr", "gespmm_csr_transpose",
     "gespmm_comm_get_unique_id", "gespmm_comm_init", "gespmm_comm_destroy", "gespmm_sharded_spmm",
     "gespmm_sharded_spmm_chunked", "gespmm_sharded_spmm_ex", "gespmm_comm_wait",
-    "gespmm_set_tma_override", "gespmm_plan_last_variant",
+    "gespmm_plan_last_variant",
 ]
 
 _i64 = ctypes.c_int64
@@ -87,7 +87,6 @@ def load():
         "gespmm_variant_name": ([_i64, _vp, _i64, _vp, _i64, _int], ctypes.c_char_p),
         "gespmm_set_variant_override": ([ctypes.c_char_p], _int),
         "gespmm_set_panel_override": ([_i64], _int),
-        "gespmm_set_tma_override": ([_int, _i64], _int),
         "gespmm_plan_last_variant": ([_vp], ctypes.c_char_p),
         "gespmm_panel_width": ([_i64, _i64], _i64),
         "gespmm_set_schedule_override": ([_int], _int),

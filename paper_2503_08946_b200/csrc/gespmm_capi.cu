@@ -228,43 +228,6 @@ int64_t g_panel_override = [] {
   return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(-1);
 }();
 
-// TMA ring (gespmm_kernel.cuh): -1 auto (the 128-column ring tile when B's
-// K x 128 slab exceeds the L2 budget -- the DRAM-bound regime the hot set is
-// for), 0 off, 1 on wherever the ring tile runs (tests).  GESPMM_TMA=<mode>.
-int g_tma_override = [] {
-  const char* e = std::getenv("GESPMM_TMA");
-  return e ? std::atoi(e) : -1;
-}();
-// hot-set size in B rows: -1 = GESPMM_HOT_MB of 512-byte rows, 0 = none
-// (GESPMM_HOT_ROWS=<rows>)
-int64_t g_hot_rows_override = [] {
-  const char* e = std::getenv("GESPMM_HOT_ROWS");
-  return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(-1);
-}();
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-bool encode_b_tensor(CUtensorMap* tm, const float* B, int64_t N, int64_t K, int64_t ldb) {
-  using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static const Enc enc = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return static_cast<Enc>(nullptr);
-    return reinterpret_cast<Enc>(f);
-  }();
-  if (!enc || K < 1 || K > (int64_t(1) << 31) - 1) return false;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(K)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldb) * 4};
-  const cuuint32_t box[2] = {128, 1};  // one 512-byte row per gathered row index
-  const cuuint32_t es[2] = {1, 1};
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 int64_t panel_width(int64_t K, int64_t N) {
   const int64_t forced = g_panel_override;
   if (forced == 0) return N;
@@ -361,32 +324,6 @@ gespmm_status_t execute_range(gespmm_plan_s* plan, int64_t N, const int32_t* row
     p.n_peers = n_peers;
     p.peer_shift = peer_shift;
     for (int q = 0; q < n_peers; ++q) p.peers[q] = peers[q] + c0;  // this panel's columns
-    // TMA ring with the plan's hot set (the ring tile in the DRAM-bound regime)
-    p.hot_bits = nullptr;
-    const bool tma_fits = v.ring && v.vec == 4 && v.cwm == 1 && !v.pair && p.off32 && ldb % 4 == 0 &&
-                          n % 4 == 0 && reinterpret_cast<uintptr_t>(B + c0) % 16 == 0;
-    // The hot set is a property of the structure, built once per plan and
-    // amortized over its executes: persistent plans only.  The one-shot and
-    // pipelined host entry points re-plan per call (and a chunk launch runs
-    // while later chunks' colind are still in flight), so they keep the
-    // cp.async ring (automatic mode) or run the TMA ring without hints (forced).
-    const bool persistent = !range && !plan->async_counts;
-    const bool tma_want = g_tma_override == 1 ||
-                          (g_tma_override < 0 && persistent &&
-                           plan->K * 128 * 4 > (int64_t(GESPMM_PANEL_L2_MB) << 20));
-    if (tma_fits && tma_want) {
-      const int64_t hot_rows = !persistent              ? 0
-                               : g_hot_rows_override >= 0 ? g_hot_rows_override
-                                                          : (int64_t(GESPMM_HOT_MB) << 20) / (128 * 4);
-      if (plan->hot_rows != hot_rows) {
-        st = build_hot_set(plan, colind, hot_rows, s);
-        if (st != GESPMM_OK) return st;
-      }
-      if (encode_b_tensor(&p.tmap, B + c0, n, plan->K, ldb)) {
-        v.tma = true;
-        p.hot_bits = plan->hot_bits;
-      }
-    }
     plan->last_variant = variant_name(v);
     cudaError_t e = launch_spmm(op, v, p, s);
     if (e != cudaSuccess) return cuda_fail(e, "spmm launch");
@@ -602,7 +539,6 @@ gespmm_status_t gespmm_plan_destroy(gespmm_plan_t plan) {
   if (plan->counters) cudaFree(plan->counters);
   if (plan->meta) cudaFree(plan->meta);
   if (plan->meta_host) cudaFreeHost(plan->meta_host);
-  if (plan->hot_bits) cudaFree(plan->hot_bits);
   delete plan;
   return GESPMM_OK;
 }
@@ -888,13 +824,6 @@ gespmm_status_t gespmm_set_tile_work_override(int32_t units) {
   if (units != 0 && (units < kRowCost || units > kTileWork))
     return fail(GESPMM_INVALID_ARG, "invalid argument: tile work must be 0 (auto) or in [2, 256]");
   g_tile_work_override = units;
-  return GESPMM_OK;
-}
-
-gespmm_status_t gespmm_set_tma_override(int mode, int64_t hot_rows) {
-  if (mode < -1 || mode > 1) return fail(GESPMM_INVALID_ARG, "invalid argument: TMA mode -1/0/1");
-  g_tma_override = mode;
-  g_hot_rows_override = hot_rows < 0 ? -1 : hot_rows;
   return GESPMM_OK;
 }
 

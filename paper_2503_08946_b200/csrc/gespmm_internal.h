@@ -2,7 +2,6 @@
 // the C-ABI layer.  Not part of the public boundary (include/gespmm.h is).
 #pragma once
 
-#include <cuda.h>  // CUtensorMap (the TMA gather4 ring's B descriptor)
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -53,12 +52,6 @@ constexpr int kPackShift = 40;
 #ifndef GESPMM_PANEL_MIN
 #define GESPMM_PANEL_MIN 64
 #endif
-// TMA ring hot set: the B rows of this many MB (at the 128-column tile's 512
-// bytes per row) get L2 evict_last (probe: 64 / 80 / 96 MB of R-MAT 2^24's
-// rows carry 55 / 60 / 64 % of its nonzeros; profiles/r2_tma_ring/)
-#ifndef GESPMM_HOT_MB
-#define GESPMM_HOT_MB 80
-#endif
 
 // Pipelined host path: at most this many row chunks per call.
 constexpr int kMaxChunks = 16;
@@ -84,10 +77,6 @@ struct Variant {
   int cwm = 1;
   bool pair = false;
   bool ring = false;  // B rows through the shared-memory cp.async ring (gespmm_kernel.cuh Ring)
-  // the ring filled by TMA gather4 (4 B rows per instruction, L2 hints per
-  // group of 4: the hot-set path, gespmm_kernel.cuh "TMA ring"); set per
-  // launch by execute_range (it needs the plan's K and hot set)
-  bool tma = false;
 };
 
 // Everything the SpMM kernel reads.  Passed by value (kernel parameter space).
@@ -126,13 +115,6 @@ struct KParams {
   int64_t peer_shift;
   // dynamic item distribution: one counter per column block, zero at launch
   unsigned long long* work_ctr;
-  // TMA ring (Variant::tma): the B panel as a 2-D tensor {N, K} (row stride
-  // ldb, box 128 x 1, out-of-range columns zero-filled), and the hot-set
-  // bitmap over B's rows (bit c of word c/32: row c is in the hot set; nullptr
-  // = no hot set).  The kernel parameter is __grid_constant__, so the tensor
-  // map's parameter-space address is a valid TMA descriptor address.
-  const unsigned* hot_bits;
-  alignas(64) CUtensorMap tmap;
 };
 
 // GESPMM_TRACE=1: phase timings of the host entry point and the plan build on
@@ -195,11 +177,6 @@ struct gespmm_plan_s {
   Meta* meta = nullptr;       // device (pool)
   Meta* meta_host = nullptr;  // pinned mirror, read after the caller's sync
   bool async_counts = false;
-  // hot set of B rows for the TMA ring's L2 hints (the most-referenced
-  // columns of this structure, sized for hot_rows rows); built on the device
-  // at the first TMA launch, kept with the plan
-  unsigned* hot_bits = nullptr;
-  int64_t hot_rows = -1;  // the row budget hot_bits was built for (-1: none)
   std::string last_variant;  // the kernel variant of the last execute (diagnostics)
 };
 
@@ -208,7 +185,4 @@ namespace gespmm {
 gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const int* colind,
                                  bool check_colind, cudaStream_t s);
 std::string csr_error_message(int err, int64_t K);
-// The plan's hot set of B rows (the hot_rows most-referenced columns of its
-// structure) for the TMA ring's L2 hints (gespmm_plan.cu); hot_rows <= 0: none.
-gespmm_status_t build_hot_set(gespmm_plan_s* plan, const int* colind, int64_t hot_rows, cudaStream_t s);
 }  // namespace gespmm

@@ -386,24 +386,9 @@ struct Ring {
   static constexpr bool kSupported = CWM == 1 && VEC >= 2;  // N = 64 / 128 column tiles
 };
 
-// TMA ring (TMA = true, with RING; DESIGN.md 5.2 "TMA ring"): the ring's
-// batches of 8 B rows are fetched by one elected lane with two TMA
-// `cp.async.bulk.tensor.2d.tile::gather4` (4 rows of 512 bytes each) into a
-// per-warp 2-stage shared-memory ring, completion on an mbarrier per stage.
-// The stage's pre-scale pass tags each column with its hot-set bit (bit 31,
-// from the plan's bitmap of the most-referenced B rows); the issuing warp
-// regroups a batch's 8 rows hot-first (ballot + popc), so the first gather4
-// carries only hot rows where it can and takes an L2 evict_last policy, an
-// all-cold or mixed group evict_first; the consumer reads position u from
-// slot sigma(u).  Fold order and results are those of every other variant.
-constexpr int kTmaRows = 8;      // rows per ring batch (two gather4)
-constexpr int kTmaStages = 2;    // ring stages per warp
-constexpr int kTmaRowBytes = 512;  // the 128-column tile's B row
-constexpr int kTmaWarpBytes = kTmaStages * kTmaRows * kTmaRowBytes;
-
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS, bool TMA = false>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinBlocks<VEC * CWM>::value)
-    spmm_kernel(const __grid_constant__ KParams P) {
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC * CWM>::value)
+    spmm_kernel(const KParams P) {
   using SR = Semiring<OP>;
   // sum/mean: two FMA chains per row (even/odd offsets from the row start),
   // held in accumulator slots by absolute position parity (batches are
@@ -412,8 +397,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
   // even chain).  max/min: one chain in slot 0.
   constexpr bool TWO = SR::kFma2;
   constexpr int CPL = VEC * CWM;       // fp32 columns per lane
-  static_assert(!TMA || (RING && VEC == 4 && CWM == 1 && OFF32), "TMA ring: the 128-column tile, 32-bit offsets");
-  constexpr int U = TMA ? kTmaRows : RING ? Ring<VEC, CWM>::U : Pipe<CPL, OP>::U;  // gathers per batch
+  constexpr int U = RING ? Ring<VEC, CWM>::U : Pipe<CPL, OP>::U;  // gathers per batch
   constexpr int FB = RING ? 0 : CPL == 1 ? GESPMM_FAST_VEC1 : CPL == 2 ? GESPMM_FAST_VEC2 : 0;  // in-row fast batch
   using RG = Ring<VEC, CWM>;
   static_assert(!RING || RG::kSupported, "ring mode: CWM == 1, VEC >= 2");
@@ -427,11 +411,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
   __shared__ __align__(16) float sval[kWarpsPerBlock][kStageCap];
 #endif
   __shared__ int rpw[kWarpsPerBlock][kTileMaxRows + 4];
-  // TMA ring: an mbarrier per stage, the issuing lane's row list, and each
-  // stage's position -> slot map (sigma)
-  __shared__ __align__(8) uint64_t tbar[TMA ? kWarpsPerBlock : 1][kTmaStages];
-  __shared__ __align__(16) int tscr[TMA ? kWarpsPerBlock : 1][kTmaRows];
-  __shared__ __align__(16) int tsig[TMA ? kWarpsPerBlock : 1][kTmaStages][kTmaRows];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -463,8 +442,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
   // ring: this lane copies 16-byte chunk (lane % kLanesPerRow) of row
   // (lane / kLanesPerRow) of every kRowsPerIssue-row group; a chunk past N
   // copies column 0 (valid memory, never read back)
-  extern __shared__ __align__(128) float4 ring_smem[];
-  float4* const ring = ring_smem + warp * (TMA ? kTmaWarpBytes / 16 : RING ? RG::kWarpBytes / 16 : 0);
+  extern __shared__ float4 ring_smem[];
+  float4* const ring = ring_smem + warp * (RING ? RG::kWarpBytes / 16 : 0);
   const int rchunk = lane % RG::kLanesPerRow;
   const int rsub = RG::kLanesPerRow >= 32 ? 0 : lane / RG::kLanesPerRow;
   // the ring's 32-bit shared-window address, and B + this lane's column
@@ -476,15 +455,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
     const int64_t c = static_cast<int64_t>(cb) * TW + 4 * rchunk;
     return c < P.N ? c : 0;
   }());
-  uint32_t tph = 0;  // TMA ring: the parity each stage's mbarrier completes next (bit d)
-  uint32_t tk = 0;   // TMA ring: batches issued so far by this warp (stage = tk % 2)
-  if constexpr (TMA) {
-    if (lane < kTmaStages)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(&tbar[warp][lane]))));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-  }
 #if GESPMM_SADDR
   int* const sc = stg[warp];
   float* const sv = reinterpret_cast<float*>(stg[warp] + kStageCap);
@@ -687,28 +657,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
     const int send = sbase + ((hi - sbase + U - 1) / U) * U;
     cp_async_wait_all();
     if (!P.idx_aligned) __syncwarp();  // 4-byte copies: other lanes own the entries
-    if constexpr (TMA) {
-      // the TMA ring gathers by row index: keep the column, tag it with its
-      // hot-set bit (bit 31); pad [hi, send) and head [sbase, lo) -> row 0
-      // (valid, never folded), as in the offset pass below
-      const int pad = hi - sbase, head = lo - sbase;
-      const unsigned* const hb = P.hot_bits;
-      auto tag = [&](int j, int c) {
-        if (j < head || j >= pad) return 0;
-        if (!hb) return c;
-        const unsigned w = __ldg(hb + (static_cast<unsigned>(c) >> 5));
-        return ((w >> (c & 31)) & 1u) ? static_cast<int>(static_cast<unsigned>(c) | 0x80000000u) : c;
-      };
-      for (int i = 4 * lane; i < send - sbase; i += 128) {
-        int4 c = *reinterpret_cast<int4*>(sc + i);
-        c.x = tag(i + 0, c.x);
-        c.y = tag(i + 1, c.y);
-        c.z = tag(i + 2, c.z);
-        c.w = tag(i + 3, c.w);
-        *reinterpret_cast<int4*>(sc + i) = c;
-      }
-      __syncwarp();
-    } else if (OFF32 && GESPMM_MERGED_PAD) {
+    if (OFF32 && GESPMM_MERGED_PAD) {
       // one pass: col -> B-row element offset col*ldb, and the pad [hi, send)
       // -> 0 (offset 0: a valid row, never folded; it overwrites whatever
       // neighbours cp.async brought in).  Each lane rewrites exactly the 4
@@ -850,76 +799,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
         fold(u & 1, v[u], b[u]);
       }
     };
-    if constexpr (TMA) {
-     if (lo < hi) {
-      // ---- TMA gather4 ring (see kTmaRows): batch j -> stage (tk + j) % 2 ----
-      const int nb = (send - sbase) / U;
-      const uint64_t pl = policy_evict_last(), pf = policy_evict_first();
-      const int ccol = cb * 128;  // this column block's first column in the tensor
-      auto tma_issue = [&](int j) {
-        const int qb = sbase + j * U;
-        const int d = static_cast<int>((tk + j) & 1u);
-        // lanes < 8: position qb + lane; regroup the batch hot-first
-        const int e = lane < U ? sc[qb - sbase + lane] : 0;
-        const unsigned hm = __ballot_sync(0xffffffffu, lane < U && e < 0);
-        const int nh = __popc(hm);
-        const unsigned lt = (1u << lane) - 1u;
-        const int slot = e < 0 ? __popc(hm & lt) : nh + __popc(~hm & lt & ((1u << U) - 1u));
-        if (lane < U) {
-          tscr[warp][slot] = e & 0x7fffffff;
-          tsig[warp][d][lane] = slot;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&tbar[warp][d]));
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                       "r"(U * kTmaRowBytes)
-                       : "memory");
-#pragma unroll
-          for (int g = 0; g < U / 4; ++g) {
-            const int4 r = *reinterpret_cast<const int4*>(&tscr[warp][4 * g]);
-            const int hot_in = min(max(nh - 4 * g, 0), 4);  // hot rows in this group
-            const uint64_t pol = hot_in == 4 ? pl : pf;
-            const uint32_t dst = ring_s + static_cast<uint32_t>((d * U + 4 * g) * kTmaRowBytes);
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-                ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
-                "l"(reinterpret_cast<uint64_t>(&P.tmap)), "r"(ccol), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w),
-                "r"(bar), "l"(pol)
-                : "memory");
-          }
-        }
-        __syncwarp();  // tscr is rewritten by the next issue
-      };
-      if (nb > 0) tma_issue(0);
-      for (int k = 0; k < nb; ++k) {
-        if (k + 1 < nb) tma_issue(k + 1);
-        const int d = static_cast<int>((tk + k) & 1u);
-        const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&tbar[warp][d]));
-        const uint32_t par = (tph >> d) & 1u;
-        uint32_t done = 0;
-        do {
-          asm volatile(
-              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-              : "=r"(done)
-              : "r"(bar), "r"(par)
-              : "memory");
-        } while (!done);
-        tph ^= 1u << d;
-        const int4 s0 = *reinterpret_cast<const int4*>(&tsig[warp][d][0]);
-        const int4 s1 = *reinterpret_cast<const int4*>(&tsig[warp][d][4]);
-        const int sg[U] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-        float ba[U][CWM][VEC];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          lds_vec<VEC>(ba[u][0], ring_s + static_cast<uint32_t>((d * U + sg[u]) * kTmaRowBytes + lane * VEC * 4));
-        consume(sbase + k * U, ba);
-        __syncwarp();  // every lane's ring reads of stage d are done ...
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ... before TMA rewrites it
-      }
-      tk += static_cast<uint32_t>(nb);
-     }
-    } else {
     if (RING && lo < hi) {
       constexpr int D = RG::kDepth;
       const int nb = (send - sbase) / U;
@@ -975,7 +854,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
         }
       }
     }
-    }  // not TMA
 
     if (is_tile) {
       // ---- the row in progress and any trailing empty rows -------------------
@@ -1058,11 +936,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TMA ? 2 : RING ? 3 : MinB
 #undef GESPMM_NEXT_ITEM
 }
 
-template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS = false, bool TMA = false>
+template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS = false>
 cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   int64_t blocks = (p.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks == 0) return cudaSuccess;
-  const int smem = TMA ? kWarpsPerBlock * kTmaWarpBytes : RING ? kWarpsPerBlock * Ring<VEC, CWM>::kWarpBytes : 0;
+  const int smem = RING ? kWarpsPerBlock * Ring<VEC, CWM>::kWarpBytes : 0;
   // persistent grid: every resident CTA slot once (per column block)
   static thread_local int cached_dev = -1, cached_slots = 0;
   int dev = 0;
@@ -1071,9 +949,9 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (RING)
-      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS, TMA>,
+      cudaFuncSetAttribute(spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS, TMA>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS>,
                                                   kWarpsPerBlock * 32, smem);
     cached_slots = sms * (per_sm > 0 ? per_sm : 1);
     cached_dev = dev;
@@ -1081,7 +959,7 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   const int64_t slots = (cached_slots + p.ncb - 1) / p.ncb;
   if (blocks > slots) blocks = slots;
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(p.ncb), 1);
-  spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS, TMA><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
+  spmm_kernel<OP, VEC, CWM, OFF32, RING, PEERS><<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1098,9 +976,6 @@ cudaError_t launch_off(const Variant& v, const KParams& p, cudaStream_t s) {
   }
   const bool ring = v.ring && OFF32 && p.ldb % 4 == 0 && p.N % 4 == 0 &&
                     reinterpret_cast<uintptr_t>(p.B) % 16 == 0;
-  if constexpr (OFF32) {
-    if (ring && v.tma && v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, true, true, false, true>(p, s);
-  }
   if (ring && v.vec == 4 && v.cwm == 1) return launch_t<OP, 4, 1, OFF32, true>(p, s);
   if (ring && v.vec == 2 && v.cwm == 1) return launch_t<OP, 2, 1, OFF32, true>(p, s);
   if (v.vec == 4 && v.cwm == 2) return launch_t<OP, 4, 2, OFF32, false>(p, s);

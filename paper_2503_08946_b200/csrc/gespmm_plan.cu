@@ -22,7 +22,6 @@
 // The reference validates the same CSR rules on the host (src/oracle.cpp:291-316).
 #include <cub/device/device_scan.cuh>
 
-#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -493,129 +492,6 @@ gespmm_status_t build_plan_async(gespmm_plan_s* plan, const int* rowptr, const i
   ce = cudaGetLastError();
   cudaFreeAsync(arena, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "plan build");
-  return GESPMM_OK;
-}
-
-// ---- hot set of B rows for the TMA ring's L2 hints --------------------------
-// The `hot_rows` most-referenced columns of the structure (B rows whose
-// gathers carry L2 evict_last; DESIGN.md 5.2 "TMA ring"): column degrees by
-// atomics, a degree histogram, the smallest threshold T whose count of
-// columns with degree >= T fits the budget, and the bitmap deg >= T.  Runs on
-// the stream with no host sync, once per plan and budget.
-namespace {
-constexpr int kDegBins = 65536;  // degrees >= kDegBins - 1 share the last bin
-
-__global__ void k_col_degree(const int* __restrict__ colind, int64_t nnz, int64_t K, int* deg) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz; p += stride) {
-    const int c = __ldg(colind + p);
-    if (c >= 0 && c < K) atomicAdd(deg + c, 1);
-  }
-}
-
-__global__ void k_degree_hist(const int* __restrict__ deg, int64_t K, int* hist) {
-  constexpr int kLocal = 2048;  // low degrees (most columns) counted in shared memory first
-  __shared__ int h[kLocal];
-  for (int i = threadIdx.x; i < kLocal; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < K; c += stride) {
-    const int d = min(deg[c], kDegBins - 1);
-    if (d <= 0) continue;
-    if (d < kLocal) atomicAdd(h + d, 1);
-    else atomicAdd(hist + d, 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kLocal; i += blockDim.x)
-    if (h[i]) atomicAdd(hist + i, h[i]);
-}
-
-// one block of 1024 threads, 64 bins each: T = 1 + the largest degree b with
-// count(deg >= b) > budget (1 when every referenced column fits)
-__global__ void __launch_bounds__(1024) k_hot_threshold(const int* __restrict__ hist, int64_t budget, int* T) {
-  constexpr int kPer = kDegBins / 1024;
-  __shared__ long long part[1024];
-  __shared__ int tmax;
-  const int t = threadIdx.x;
-  long long sum = 0;
-  for (int b = t * kPer; b < (t + 1) * kPer; ++b) sum += hist[b];
-  part[t] = sum;
-  if (t == 0) tmax = 0;
-  __syncthreads();
-  if (t == 0) {  // exclusive suffix sums: columns in the bins above each thread's range
-    long long run = 0;
-    for (int i = 1023; i >= 0; --i) {
-      const long long x = part[i];
-      part[i] = run;
-      run += x;
-    }
-  }
-  __syncthreads();
-  long long run = part[t];
-  if (run <= budget) {
-    for (int b = (t + 1) * kPer - 1; b >= t * kPer; --b) {
-      run += hist[b];
-      if (run > budget) {
-        atomicMax(&tmax, b);
-        break;
-      }
-    }
-  }
-  __syncthreads();
-  if (t == 0) *T = tmax + 1;
-}
-
-__global__ void k_hot_bits(const int* __restrict__ deg, int64_t K, const int* __restrict__ T, unsigned* bits) {
-  const int thr = *T;
-  const int64_t words = (K + 31) / 32;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < words; w += stride) {
-    unsigned m = 0;
-    for (int j = 0; j < 32; ++j) {
-      const int64_t c = 32 * w + j;
-      if (c < K) {
-        const int d = deg[c];
-        if (d > 0 && d >= thr) m |= 1u << j;
-      }
-    }
-    bits[w] = m;
-  }
-}
-}  // namespace
-
-gespmm_status_t build_hot_set(gespmm_plan_s* plan, const int* colind, int64_t hot_rows, cudaStream_t s) {
-  if (plan->hot_bits) cudaFreeAsync(plan->hot_bits, s);
-  plan->hot_bits = nullptr;
-  plan->hot_rows = hot_rows;
-  if (hot_rows <= 0 || plan->K == 0) return GESPMM_OK;
-  const int64_t K = plan->K, words = (K + 31) / 32;
-  int *deg = nullptr, *hist = nullptr;
-  cudaError_t e = cudaMallocAsync(&plan->hot_bits, static_cast<size_t>(words) * 4, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&deg, static_cast<size_t>(K) * 4, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&hist, static_cast<size_t>(kDegBins + 1) * 4, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(deg, 0, static_cast<size_t>(K) * 4, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, static_cast<size_t>(kDegBins + 1) * 4, s);
-  if (e == cudaSuccess && plan->nnz > 0) {
-    const int64_t g = std::min<int64_t>((plan->nnz + 255) / 256, 148 * 16);
-    k_col_degree<<<static_cast<unsigned>(g), 256, 0, s>>>(colind, plan->nnz, K, deg);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) {
-    const int64_t g = std::min<int64_t>((K + 255) / 256, 148 * 8);
-    k_degree_hist<<<static_cast<unsigned>(g), 256, 0, s>>>(deg, K, hist);
-    k_hot_threshold<<<1, 1024, 0, s>>>(hist, hot_rows, hist + kDegBins);
-    const int64_t gw = std::min<int64_t>((words + 255) / 256, 148 * 8);
-    k_hot_bits<<<static_cast<unsigned>(gw), 256, 0, s>>>(deg, K, hist + kDegBins, plan->hot_bits);
-    e = cudaGetLastError();
-  }
-  if (deg) cudaFreeAsync(deg, s);
-  if (hist) cudaFreeAsync(hist, s);
-  if (e != cudaSuccess) {
-    if (plan->hot_bits) cudaFreeAsync(plan->hot_bits, s);
-    plan->hot_bits = nullptr;
-    plan->hot_rows = -1;
-    return cuda_fail(e, "hot set");
-  }
   return GESPMM_OK;
 }
 

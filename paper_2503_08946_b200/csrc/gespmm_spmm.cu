@@ -27,8 +27,7 @@ int variant_cols(const Variant& v) { return v.pair ? 16 * v.vec : 32 * v.vec * v
 
 std::string variant_name(const Variant& v) {
   if (v.pair) return "pair_vec" + std::to_string(v.vec);
-  return "vec" + std::to_string(v.vec) + "_lpr32_cwm" + std::to_string(v.cwm) + (v.ring ? "_ring" : "") +
-         (v.tma ? "_tma" : "");
+  return "vec" + std::to_string(v.vec) + "_lpr32_cwm" + std::to_string(v.cwm) + (v.ring ? "_ring" : "");
 }
 
 namespace {

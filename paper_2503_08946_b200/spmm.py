@@ -89,7 +89,7 @@ class Plan:
 
     def last_variant(self) -> str:
         """The kernel variant this plan's last execute launched ("" before any),
-        e.g. "vec4_lpr32_cwm1_ring_tma" (gespmm_plan_last_variant)."""
+        e.g. "vec4_lpr32_cwm1_ring" (gespmm_plan_last_variant)."""
         return _L.gespmm_plan_last_variant(self._h).decode()
 
     def info(self) -> dict:
@@ -322,15 +322,6 @@ def set_tile_work_override(units: int = 0) -> None:
     """Tile size (work units) of plans built afterwards: 0 = automatic; results
     never depend on it.  Test/tuning knob (gespmm_set_tile_work_override)."""
     _lib.check(_L.gespmm_set_tile_work_override(int(units)))
-
-
-def set_tma_override(mode: int = -1, hot_rows: int = -1) -> None:
-    """TMA gather4 ring with an L2 hot set for the 128-column ring tile: mode
-    -1 automatic (B's K x 128 slab larger than the L2 budget, persistent plans),
-    0 off, 1 wherever the ring tile runs; hot_rows -1 automatic (80 MB of rows),
-    0 none.  Results never depend on it.  Test/tuning knob
-    (gespmm_set_tma_override)."""
-    _lib.check(_L.gespmm_set_tma_override(int(mode), int(hot_rows)))
 
 
 def set_panel_override(cols: int = -1) -> None:

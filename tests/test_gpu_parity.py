@@ -185,6 +185,10 @@ def test_every_variant_bit_exact(cuda, oracle_mod, variant, op, tile_work):
         got, plan = gpu_spmm(cuda, rowptr, colind, vals, B, op)
         if tile_work:
             assert plan.info()["tile_work"] == tile_work
+        # the variant that really ran (N=96 is a multiple of every VEC; the
+        # ring needs 16-byte B rows, so it may fall back to the register path)
+        ran = plan.last_variant()
+        assert ran == variant or (variant.endswith("_ring") and ran == variant[:-5]), ran
     finally:
         spmm.set_variant_override("")
         spmm.set_tile_work_override(0)
