@@ -266,6 +266,9 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #ifndef GESPMM_PIN
 #define GESPMM_PIN 1
 #endif
+#ifndef GESPMM_SPOS_SHFL
+#define GESPMM_SPOS_SHFL 1
+#endif
 // A value the compiler must keep in a register (an opaque move: it cannot be
 // rematerialized from the special registers / constants it came from).
 __device__ __forceinline__ uint32_t pin_reg(uint32_t x) {
@@ -713,7 +716,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     // ---- gather pipeline over 4-aligned batches [qb, qb+U) ------------------
 #if GESPMM_SADDR
     // 32-bit shared address of stage entry 0 relative to position 0
-    const uint32_t s_pos0 = sc_s - 4u * static_cast<uint32_t>(sbase);
+    // produced by a shuffle (GESPMM_SPOS_SHFL, >= 2 columns per lane), so
+    // ptxas keeps it in a register instead of rematerializing it from SR_TID /
+    // SR_CgaCtaId in every batch -- 10 instructions per batch of 12 at the
+    // 64-column tile (the opaque mov on sc_s does not survive ptxas's copy
+    // propagation).  Config 2 sum / max / mean 0.3316 / 0.3373 / 0.3697 ->
+    // 0.3261 / 0.3347 / 0.3673 ms, config 3 N=64 1.740 -> 1.727, config 5
+    // 52.23 -> 51.99; at one column per lane it lost (config 3 N=32 1.153 ->
+    // 1.170 ms; profiles/r2_spos/)
+    const uint32_t s_pos0 = (GESPMM_SPOS_SHFL && CPL >= 2)
+                                ? __shfl_sync(0xffffffffu, sc_s - 4u * static_cast<uint32_t>(sbase), 0)
+                                : sc_s - 4u * static_cast<uint32_t>(sbase);
 #endif
     // the 4 staged offsets / values at positions qb + 4g .. qb + 4g + 3
     auto stage_off4 = [&](int qb, int g) {
