@@ -269,6 +269,9 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #ifndef GESPMM_SPOS_SHFL
 #define GESPMM_SPOS_SHFL 1
 #endif
+#ifndef GESPMM_RP_SHFL
+#define GESPMM_RP_SHFL 1
+#endif
 // A value the compiler must keep in a register (an opaque move: it cannot be
 // rematerialized from the special registers / constants it came from).
 __device__ __forceinline__ uint32_t pin_reg(uint32_t x) {
@@ -709,7 +712,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
     const int64_t grow0 = it.x;  // global row of local row 0
     const int64_t ldc = P.ldc;
     float* crow = P.C + grow0 * ldc + woff[0];
-    int row = 0, rs = lo, re = is_tile ? rp[1] : hi;
+    // the rowptr window read through a 32-bit shared address that a shuffle
+    // produced (GESPMM_RP_SHFL, >= 2 columns per lane): otherwise ptxas
+    // rematerializes the window's address from SR_TID / SR_CgaCtaId at every
+    // row end.  Config 2 sum / mean 0.3267 / 0.3670 -> 0.3221 / 0.3630 ms,
+    // config 3 N=64 1.714 -> 1.710; at one column per lane (config 3 N=32)
+    // and in the paired-lane kernel it lost 0.3-0.5 % (profiles/r2_spos/)
+    const uint32_t rp_s = (GESPMM_RP_SHFL && CPL >= 2)
+                              ? __shfl_sync(0xffffffffu, static_cast<uint32_t>(__cvta_generic_to_shared(rp)), 0)
+                              : static_cast<uint32_t>(__cvta_generic_to_shared(rp));
+    auto rp_at = [&](int k) {
+      int x;
+      asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(rp_s + 4u * static_cast<uint32_t>(k)));
+      return x;
+    };
+    int row = 0, rs = lo, re = is_tile ? rp_at(1) : hi;
     if (!is_tile && it.y > 0) seed(lo, SR::identity(), nullptr);
     else row_seed(lo, crow);
 
@@ -806,7 +823,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
           ++row;
           crow += ldc;
           rs = re;
-          re = rp[row + 1];
+          re = rp_at(row + 1);
           row_seed(rs, crow);
         }
         fold(u & 1, v[u], b[u]);
@@ -875,7 +892,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         if (++row >= nr) break;
         crow += ldc;
         rs = re;
-        re = rp[row + 1];
+        re = rp_at(row + 1);
         row_seed(rs, crow);
       }
       GESPMM_NEXT_ITEM;
