@@ -272,6 +272,9 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #ifndef GESPMM_RP_SHFL
 #define GESPMM_RP_SHFL 1
 #endif
+#ifndef GESPMM_SEED_BRANCH
+#define GESPMM_SEED_BRANCH 1
+#endif
 // A value the compiler must keep in a register (an opaque move: it cannot be
 // rematerialized from the special registers / constants it came from).
 __device__ __forceinline__ uint32_t pin_reg(uint32_t x) {
@@ -498,8 +501,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
   };
   // C rows are addressed through a running pointer (crow = C + row*ldc + the
   // lane's column), advanced by ldc per row: no 64-bit multiply per row.
+  // a warp-uniform branch on the launch-wide accumulate flag, so the common
+  // (no C0) path is the chain seeds alone (GESPMM_SEED_BRANCH); the select
+  // form kept the C0 pointer test, the flag load and the predicated load at
+  // every row end (sum only -- the other ops fold C0 in at the store: config
+  // 2 sum 0.3211 -> 0.3158 ms, config 4 2.68 -> 2.64, config 3 N=64 -0.5 %;
+  // profiles/r2_spos/summary_sb.txt)
   auto row_seed = [&](int start, const float* crow_) {
-    seed(start, SR::zero(), seed_c0 ? crow_ : nullptr);
+    if (GESPMM_SEED_BRANCH) {
+      if (seed_c0) seed(start, SR::zero(), crow_);
+      else seed(start, SR::zero(), nullptr);
+    } else {
+      seed(start, SR::zero(), seed_c0 ? crow_ : nullptr);
+    }
   };
   auto value = [&](int w, int k) { return TWO ? acc[0][w][k] + acc[1][w][k] : acc[0][w][k]; };
   auto store_row = [&](float* dst, int deg) {
