@@ -275,6 +275,9 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #ifndef GESPMM_SEED_BRANCH
 #define GESPMM_SEED_BRANCH 1
 #endif
+#ifndef GESPMM_SLOW_MASK
+#define GESPMM_SLOW_MASK 1
+#endif
 // A value the compiler must keep in a register (an opaque move: it cannot be
 // rematerialized from the special registers / constants it came from).
 __device__ __forceinline__ uint32_t pin_reg(uint32_t x) {
@@ -826,6 +829,37 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
       if (qb >= lo && qb + U <= min(hi, re)) {  // fast path: U nonzeros of the current row
 #pragma unroll
         for (int u = 0; u < U; u += 2) fold_pair(v[u], b[u], v[u + 1], b[u + 1]);
+        return;
+      }
+      if (GESPMM_SLOW_MASK && U == 8) {
+        // slow path by row runs: the batch's valid positions [u0, u1) split at
+        // the row ends inside it; each run is folded under a bit mask of its
+        // positions (predicated FFMA2s in position order), rows ending at or
+        // before the run start are stored first.  One pass per row the batch
+        // touches instead of a compare-and-branch chain per position: config
+        // 2 max / mean 0.335 / 0.364 -> 0.328 / 0.348 ms, config 3 N=32 -0.4 %.
+        // Not for sum's 12-row batches at the 64-column tile, where it adds
+        // per-item spills (config 2 0.317 -> 0.311 ms, but config 3 N=64 /
+        // 256 +3 / +3.5 %, config 5 at N=64 +3 %; profiles/r2_slowmask/).
+        int u = max(lo - qb, 0);
+        const int u1 = min(hi - qb, U);
+        for (;;) {
+          while (qb + u >= re) {  // rows ending at or before position qb + u are complete (tiles only)
+            store_row(crow, re - rs);
+            ++row;
+            crow += ldc;
+            rs = re;
+            re = rp_at(row + 1);
+            row_seed(rs, crow);
+          }
+          const int e = min(re - qb, u1);  // [u, e): the current row's run
+          const unsigned m = ((1u << e) - 1u) & ~((1u << u) - 1u);
+#pragma unroll
+          for (int k = 0; k < U; ++k)
+            if ((m >> k) & 1u) fold(k & 1, v[k], b[k]);
+          if (e >= u1) break;
+          u = e;
+        }
         return;
       }
 #pragma unroll
