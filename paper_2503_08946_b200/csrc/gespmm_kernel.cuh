@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
         for (int u = 0; u < U; u += 2) fold_pair(v[u], b[u], v[u + 1], b[u + 1]);
         return;
       }
-      if (GESPMM_SLOW_MASK && U == 8) {
+      if constexpr (GESPMM_SLOW_MASK && U == 8) {
         // slow path by row runs: the batch's valid positions [u0, u1) split at
         // the row ends inside it; each run is folded under a bit mask of its
         // positions (predicated FFMA2s in position order), rows ending at or
@@ -860,21 +860,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC 
           if (e >= u1) break;
           u = e;
         }
-        return;
-      }
+      } else {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {  // slow path: element by element
-        const int p = qb + u;
-        if (p < lo || p >= hi) continue;
-        while (p >= re) {  // rows ending at or before p are complete (tiles only)
-          store_row(crow, re - rs);
-          ++row;
-          crow += ldc;
-          rs = re;
-          re = rp_at(row + 1);
-          row_seed(rs, crow);
+        for (int u = 0; u < U; ++u) {  // slow path: element by element
+          const int p = qb + u;
+          if (p < lo || p >= hi) continue;
+          while (p >= re) {  // rows ending at or before p are complete (tiles only)
+            store_row(crow, re - rs);
+            ++row;
+            crow += ldc;
+            rs = re;
+            re = rp_at(row + 1);
+            row_seed(rs, crow);
+          }
+          fold(u & 1, v[u], b[u]);
         }
-        fold(u & 1, v[u], b[u]);
       }
     };
     if (RING && lo < hi) {
