@@ -384,6 +384,12 @@ struct MinBlocks {
 // VEC = 2, U = 4 rows of 512 B at VEC = 4).  Measured ceiling on config 2's
 // column stream (tools/gather_probe.cu): 0.248 ms at 24 warps/SM vs 0.311 ms
 // for register gathers with 8 rows in flight at 32 warps/SM.
+#ifndef GESPMM_RING_U512
+#define GESPMM_RING_U512 4  // rows per ring batch at 512-byte rows
+#endif
+#ifndef GESPMM_RING_MINBLOCKS
+#define GESPMM_RING_MINBLOCKS 3
+#endif
 #ifndef GESPMM_RING_DEPTH
 #define GESPMM_RING_DEPTH 2  // ring batches (D - 1 in flight while one is folded); 3 measured slower (2 CTAs/SM)
 #endif
@@ -392,14 +398,14 @@ struct Ring {
   static constexpr int kRowBytes = 128 * VEC * CWM;     // one B row, the warp's columns
   static constexpr int kLanesPerRow = kRowBytes / 16;   // 16-byte chunks per row
   static constexpr int kRowsPerIssue = kLanesPerRow >= 32 ? 1 : 32 / kLanesPerRow;
-  static constexpr int U = kRowBytes >= 512 ? 4 : 8;
+  static constexpr int U = kRowBytes >= 512 ? GESPMM_RING_U512 : 8;
   static constexpr int kDepth = GESPMM_RING_DEPTH;
   static constexpr int kWarpBytes = kDepth * U * kRowBytes;
   static constexpr bool kSupported = CWM == 1 && VEC >= 2;  // N = 64 / 128 column tiles
 };
 
 template <gespmm_reduce_t OP, int VEC, int CWM, bool OFF32, bool RING, bool PEERS>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? 3 : MinBlocks<VEC * CWM>::value)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLOCKS : MinBlocks<VEC * CWM>::value)
     spmm_kernel(const KParams P) {
   using SR = Semiring<OP>;
   // sum/mean: two FMA chains per row (even/odd offsets from the row start),
