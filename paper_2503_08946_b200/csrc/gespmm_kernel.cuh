@@ -45,6 +45,8 @@
 //    the result is deterministic and needs no second launch.
 #pragma once
 
+#include <type_traits>
+
 #include "gespmm_internal.h"
 #include "gespmm_semiring.cuh"
 
@@ -277,6 +279,12 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #endif
 #ifndef GESPMM_SLOW_MASK
 #define GESPMM_SLOW_MASK 1
+#endif
+#ifndef GESPMM_ITEM32
+#define GESPMM_ITEM32 1
+#endif
+#ifndef GESPMM_SLOW_MASK_U12
+#define GESPMM_SLOW_MASK_U12 0
 #endif
 // A value the compiler must keep in a register (an opaque move: it cannot be
 // rematerialized from the special registers / constants it came from).
@@ -599,16 +607,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLO
   // Persistent warps: warp-strided walk over the work list (no warp idles while
   // a sibling in its CTA finishes a longer item).  Control flow is warp-uniform
   // and the kernel uses no CTA-wide barrier.
-  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
+  // Item indices fit 32 bits (a plan has < 2^29 items: nnz < 2^31 and a tile
+  // holds >= 16 work units), so the item cursor, its bounds and the grabbed
+  // index are 32-bit (GESPMM_ITEM32): fewer registers live across the item
+  // (config 2 sum / max -0.9 / -0.6 %, config 3 N=16/32/64 -0.3/-1.2/-1.0 %;
+  // mean lost 1.2 % and keeps 64-bit; profiles/r2_spos/summary_i32.txt)
+  constexpr bool kItem32 = GESPMM_ITEM32 != 0 && OP != GESPMM_REDUCE_MEAN;
+  using item_t = std::conditional_t<kItem32, int, int64_t>;
+  using grab_t = std::conditional_t<kItem32, unsigned, unsigned long long>;
+  const item_t wstride = static_cast<item_t>(gridDim.x) * kWarpsPerBlock;
   // the item count: on the device for plans built without a host sync
   const int64_t n_items = P.n_items_dev ? *P.n_items_dev : P.n_items;
-  int64_t t_begin = 0, t_end = n_items;
+  item_t t_begin = 0, t_end = static_cast<item_t>(n_items);
   // a failed on-device colind check earlier on the stream (host entry point,
   // single- or multi-chunk): no item is gathered through an invalid colind
   if (P.abort_flag && *reinterpret_cast<const volatile int*>(P.abort_flag)) return;
   if (P.range) {  // one chunk of the pipelined host path
-    t_begin = P.range[0];
-    t_end = P.range[1];
+    t_begin = static_cast<item_t>(P.range[0]);
+    t_end = static_cast<item_t>(P.range[1]);
   }
   // Item distribution: dynamic when the launch carries a counter (P.work_ctr,
   // zeroed before the launch; one per column block): warps grab items with an
@@ -620,20 +636,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLO
   // 57.5 -> 49.6 ms.
 #define GESPMM_NEXT_ITEM                                                         \
   {                                                                              \
-    t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(0xffffffffu, next, 0)) : t + wstride; \
+    t = dyn ? t_begin + static_cast<item_t>(__shfl_sync(0xffffffffu, next, 0)) : t + wstride; \
     continue;                                                                    \
   }
   const bool dyn = P.work_ctr != nullptr;
   unsigned long long* const wctr = dyn ? P.work_ctr + blockIdx.y : nullptr;
   auto grab = [&]() {
-    unsigned long long v = 0;
-    if (lane == 0) v = atomicAdd(wctr, 1ULL);
+    grab_t v = 0;
+    if (lane == 0) v = static_cast<grab_t>(atomicAdd(wctr, 1ULL));
     return v;
   };
-  int64_t t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(0xffffffffu, grab(), 0))
-                  : t_begin + static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  item_t t = dyn ? t_begin + static_cast<item_t>(__shfl_sync(0xffffffffu, grab(), 0))
+                 : t_begin + static_cast<item_t>(blockIdx.x) * kWarpsPerBlock + warp;
   for (; t < t_end;) {
-    const unsigned long long next = dyn ? grab() : 0ULL;
+    const grab_t next = dyn ? grab() : grab_t(0);
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];
     const bool is_tile = it.y < 0;
@@ -837,7 +853,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLO
         for (int u = 0; u < U; u += 2) fold_pair(v[u], b[u], v[u + 1], b[u + 1]);
         return;
       }
-      if constexpr (GESPMM_SLOW_MASK && U == 8) {
+      if constexpr (GESPMM_SLOW_MASK && (U == 8 || (GESPMM_SLOW_MASK_U12 && U == 12))) {
         // slow path by row runs: the batch's valid positions [u0, u1) split at
         // the row ends inside it; each run is folded under a bit mask of its
         // positions (predicated FFMA2s in position order), rows ending at or
@@ -1015,7 +1031,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLO
     }
     store_row(crow, deg);
     if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
-    t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(0xffffffffu, next, 0)) : t + wstride;
+    t = dyn ? t_begin + static_cast<item_t>(__shfl_sync(0xffffffffu, next, 0)) : t + wstride;
   }  // item loop
 #undef GESPMM_NEXT_ITEM
 }

@@ -135,16 +135,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     }
   };
 
-  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
+  // 32-bit item cursor (GESPMM_ITEM32; gespmm_kernel.cuh)
+  constexpr bool kItem32 = GESPMM_ITEM32 != 0 && OP != GESPMM_REDUCE_MEAN;
+  using item_t = std::conditional_t<kItem32, int, int64_t>;
+  using grab_t = std::conditional_t<kItem32, unsigned, unsigned long long>;
+  const item_t wstride = static_cast<item_t>(gridDim.x) * kWarpsPerBlock;
   // the item count: on the device for plans built without a host sync
   const int64_t n_items = P.n_items_dev ? *P.n_items_dev : P.n_items;
-  int64_t t_begin = 0, t_end = n_items;
+  item_t t_begin = 0, t_end = static_cast<item_t>(n_items);
   // a failed on-device colind check earlier on the stream (host entry point,
   // single- or multi-chunk): no item is gathered through an invalid colind
   if (P.abort_flag && *reinterpret_cast<const volatile int*>(P.abort_flag)) return;
   if (P.range) {  // one chunk of the pipelined host path
-    t_begin = P.range[0];
-    t_end = P.range[1];
+    t_begin = static_cast<item_t>(P.range[0]);
+    t_end = static_cast<item_t>(P.range[1]);
   }
   // Item distribution: dynamic when the launch carries a counter (P.work_ctr,
   // zeroed before the launch; one per column block): warps grab items with an
@@ -156,20 +160,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
   // 57.5 -> 49.6 ms.
 #define GESPMM_NEXT_ITEM                                                         \
   {                                                                              \
-    t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(FULL, next, 0)) : t + wstride; \
+    t = dyn ? t_begin + static_cast<item_t>(__shfl_sync(FULL, next, 0)) : t + wstride; \
     continue;                                                                    \
   }
   const bool dyn = P.work_ctr != nullptr;
   unsigned long long* const wctr = dyn ? P.work_ctr + blockIdx.y : nullptr;
   auto grab = [&]() {
-    unsigned long long v = 0;
-    if (lane == 0) v = atomicAdd(wctr, 1ULL);
+    grab_t v = 0;
+    if (lane == 0) v = static_cast<grab_t>(atomicAdd(wctr, 1ULL));
     return v;
   };
-  int64_t t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(FULL, grab(), 0))
-                  : t_begin + static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  item_t t = dyn ? t_begin + static_cast<item_t>(__shfl_sync(FULL, grab(), 0))
+                 : t_begin + static_cast<item_t>(blockIdx.x) * kWarpsPerBlock + warp;
   for (; t < t_end;) {
-    const unsigned long long next = dyn ? grab() : 0ULL;
+    const grab_t next = dyn ? grab() : grab_t(0);
     __syncwarp();  // the previous item's stage reads are done (the role of mir:65)
     const int4 it = P.items[t];
     const bool is_tile = it.y < 0;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
       Vec<VEC>::stcs(crow, r);
     }
     if (lane == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
-    t = dyn ? t_begin + static_cast<int64_t>(__shfl_sync(FULL, next, 0)) : t + wstride;
+    t = dyn ? t_begin + static_cast<item_t>(__shfl_sync(FULL, next, 0)) : t + wstride;
   }  // item loop
 #undef GESPMM_NEXT_ITEM
 }
