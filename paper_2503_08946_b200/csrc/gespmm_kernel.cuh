@@ -283,6 +283,9 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #ifndef GESPMM_ITEM32
 #define GESPMM_ITEM32 1
 #endif
+#ifndef GESPMM_RING_NOSYNC
+#define GESPMM_RING_NOSYNC 1
+#endif
 #ifndef GESPMM_SLOW_MASK_U12
 #define GESPMM_SLOW_MASK_U12 0
 #endif
@@ -911,12 +914,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLO
         if (k + D - 1 < nb) issue_ring(sbase + (k + D - 1) * U, (k + D - 1) % D);
         else asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
-        __syncwarp();  // every lane's chunks of batch k are in the ring
+        // At 512-byte rows (kLanesPerRow = 32) lane l copies and later reads
+        // exactly bytes [16l, 16l + 16) of every row: its own wait_group
+        // orders them and no other lane touches them, so the ring needs no
+        // warp barrier (GESPMM_RING_NOSYNC); narrower rows map a lane's copy
+        // and its read to different bytes and keep both barriers.  (Measured
+        // neutral on the DRAM-bound configs 4/5, -0.3 to -0.6 % on config 4
+        // sum/mean; racecheck clean: profiles/r2_ring_nosync/.)
+        constexpr bool kOwn = GESPMM_RING_NOSYNC && RG::kLanesPerRow == 32 && RG::kRowsPerIssue == 1;
+        if (!kOwn) __syncwarp();  // every lane's chunks of batch k are in the ring
         float ba[U][CWM][VEC];
 #pragma unroll
         for (int u = 0; u < U; ++u) ring_row(k % D, u, ba[u]);
         consume(sbase + k * U, ba);
-        __syncwarp();  // slot k % D is refilled at iteration k + 1
+        if (!kOwn) __syncwarp();  // slot k % D is refilled at iteration k + 1
       }
     } else if (lo < hi) {
       {
