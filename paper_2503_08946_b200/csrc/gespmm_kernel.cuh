@@ -359,12 +359,15 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // more rows in flight for a 24-byte spill outside the batch loop -- config 4 /
 // 5 at N=64 1.467 -> 1.416 / 26.3 -> 25.7 ms, config 2 0.335 -> 0.332 ms;
 // max lost (0.338 -> 0.343 ms), so the other ops keep 8 (profiles/r2_pin/r2_c30_*)
+#ifndef GESPMM_U_VEC4
+#define GESPMM_U_VEC4 4  // register batch at four columns per lane (the ring runs that tile by default)
+#endif
 #ifndef GESPMM_U_SUM2
 #define GESPMM_U_SUM2 12
 #endif
 template <int CPL, gespmm_reduce_t OP>
 struct Pipe {
-  static constexpr int U = CPL >= 4 ? 4 : (CPL == 2 && OP == GESPMM_REDUCE_SUM) ? GESPMM_U_SUM2 : GESPMM_U_NARROW;
+  static constexpr int U = CPL >= 8 ? 4 : CPL == 4 ? GESPMM_U_VEC4 : (CPL == 2 && OP == GESPMM_REDUCE_SUM) ? GESPMM_U_SUM2 : GESPMM_U_NARROW;
 };
 
 #ifndef GESPMM_MINBLOCKS
@@ -382,10 +385,13 @@ struct Pipe {
 #ifndef GESPMM_MINBLOCKS_ONE
 #define GESPMM_MINBLOCKS_ONE GESPMM_MINBLOCKS  // 1 column per lane (N <= 32 tiles)
 #endif
+#ifndef GESPMM_MINBLOCKS_VEC4
+#define GESPMM_MINBLOCKS_VEC4 GESPMM_MINBLOCKS
+#endif
 template <int CPL>
 struct MinBlocks {
   static constexpr int value =
-      CPL >= 8 ? GESPMM_MINBLOCKS_WIDE : (CPL == 1 ? GESPMM_MINBLOCKS_ONE : GESPMM_MINBLOCKS);
+      CPL >= 8 ? GESPMM_MINBLOCKS_WIDE : (CPL == 1 ? GESPMM_MINBLOCKS_ONE : CPL == 4 ? GESPMM_MINBLOCKS_VEC4 : GESPMM_MINBLOCKS);
 };
 
 // Ring mode (RING = true; DESIGN.md 5.2 "Gather ring"): B rows are copied
