@@ -1,3 +1,4 @@
+# device timeline of the pipelined host entry point (GESPMM_TRACE=3) on config 2: per-chunk H2D / kernel / D2H completion times (profiles/r1_e2e_timeline.txt)
 mkdir -p gpurun_out
 GESPMM_TRACE=3 python -c "
 import torch,sys

@@ -1,3 +1,4 @@
+# round 1 final: ncu --set full of the SpMM kernel on configs 2 (sum, max), 3 (N=64), 4, 5 and the launch list of the default bench command (profiles/r1_*_final_ncu.txt)
 mkdir -p gpurun_out
 export GESPMM_NO_PROBE=1
 prof() { tag=$1; w=$2; op=$3

@@ -1,3 +1,4 @@
+# round 2, probe: the GPU box itself (memory, cores, SM clock, L2 size, SM count)
 set -x
 free -g; nproc; nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv
 python -c "import torch;p=torch.cuda.get_device_properties(0);print(p.L2_cache_size, p.multi_processor_count)"
