@@ -30,6 +30,9 @@ namespace kern {
 #ifndef GESPMM_PAIR_U
 #define GESPMM_PAIR_U 16  // measured: config 3 N=16 1.356 -> 1.255 ms vs 8
 #endif
+#ifndef GESPMM_SPOS_SHFL_PAIR
+#define GESPMM_SPOS_SHFL_PAIR 1
+#endif
 #ifndef GESPMM_PAIR_U1
 #define GESPMM_PAIR_U1 GESPMM_PAIR_U  // one column per lane (N <= 16)
 #endif
@@ -272,7 +275,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GESPMM_PAIR_MINBLOCKS)
     else row_seed(lo, crow);
 
     // 32-bit shared address of my half's entries of 8-entry block 0
-    const uint32_t s_pos0 = sc_s + 4u * static_cast<uint32_t>(4 * g - sbase);
+    // through a shuffle (GESPMM_SPOS_SHFL_PAIR, one column per lane): ptxas
+    // otherwise recomputes the half's offset from SR_TID in every batch
+    // (DESIGN.md 5.2 item 11): config 3 N=16 sum / max / mean 1.071 / 1.090 /
+    // 1.083 -> 1.040 / 1.057 / 1.051 ms; pair_vec2 (N=32 max) +0.3 %, so not there
+    const uint32_t s_pos0 = (GESPMM_SPOS_SHFL_PAIR && VEC == 1)
+                                ? __shfl_sync(FULL, sc_s + 4u * static_cast<uint32_t>(4 * g - sbase), lane)
+                                : sc_s + 4u * static_cast<uint32_t>(4 * g - sbase);
     for (int qb = sbase; qb < hi; qb += U) {
       // my half's staged entries of this batch, four per 8-entry block:
       // entry i is position qb + 2i + g
