@@ -659,12 +659,19 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
   // the host first, so the D2H stream starts right after B arrives and the
   // heavy chunks' H2D overlaps the C drain (PCIe is full duplex).  R-MAT puts
   // a third of the nonzeros in the first 1/16 of the rows; in row order the
-  // D2H stream idled behind them (11.3 ms).
+  // D2H stream idled behind them (11.3 ms).  Chunks of equal
+  // PCIe bytes (8 rowptr[i] + 4 N i; GESPMM_HOST_EQUAL_BYTES=1) shrink the
+  // last chunk's tail but measured no better: after B the call is bound by
+  // duplex PCIe (config 5: 8.2 GB in + 8.6 GB out at ~45 GB/s each way),
+  // 354.8 vs 358.6 ms on config 5, 83.0 vs 80.7 on config 4, 11.0 vs 10.8 on
+  // config 2 (profiles/r2_chunks/).
   const int64_t c_bytes = M * N * 4;
-  int nc = static_cast<int>(c_bytes / (8 << 20));
+  int nc = static_cast<int>(std::min<int64_t>(c_bytes / (8 << 20), 16));
+  if (const char* x = std::getenv("GESPMM_HOST_CHUNKS")) nc = std::atoi(x);  // tests / A/B, <= kMaxChunks
   if (nc > kMaxChunks) nc = kMaxChunks;
   if (nc < 1 || std::getenv("GESPMM_HOST_NO_PIPELINE")) nc = 1;
   const bool in_row_order = std::getenv("GESPMM_HOST_ROW_ORDER") != nullptr;  // A/B switch
+  const bool equal_rows = std::getenv("GESPMM_HOST_EQUAL_BYTES") == nullptr;
   // A launch reads its item's colind/vals up to the 16-byte staging granule
   // past the item end (never folded); chunk transfers cover that overhang.
   const int64_t overhang = 16;
@@ -714,7 +721,24 @@ gespmm_status_t gespmm_csr_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nn
     return e != cudaSuccess ? cuda_fail(e, "plan") : st;
   }
   int64_t rows[kMaxChunks + 1];
-  for (int c = 0; c <= nc; ++c) rows[c] = M * c / nc;
+  if (equal_rows) {
+    for (int c = 0; c <= nc; ++c) rows[c] = M * c / nc;
+  } else {  // first row i with cost(i) >= c / nc of the total (host rowptr)
+    const int64_t wr = 4 * N;
+    auto cost = [&](int64_t i) { return 8 * static_cast<int64_t>(rowptr[i]) + wr * i; };
+    const int64_t total = cost(M);
+    rows[0] = 0;
+    for (int c = 1; c <= nc; ++c) {
+      const int64_t target = static_cast<int64_t>(static_cast<double>(total) * c / nc);
+      int64_t lo = rows[c - 1], hi = M;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cost(mid) < target) lo = mid + 1;
+        else hi = mid;
+      }
+      rows[c] = c == nc ? M : lo;
+    }
+  }
   chk(chunk_rows_aligned(plan, rows, nc, d_ranges, d_rows, s));
   chk(cudaMemcpyAsync(rows, d_rows, static_cast<size_t>(nc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   chk(cudaStreamSynchronize(s));  // ~20 us; B is still in flight

@@ -54,7 +54,7 @@ constexpr int kPackShift = 40;
 #endif
 
 // Pipelined host path: at most this many row chunks per call.
-constexpr int kMaxChunks = 16;
+constexpr int kMaxChunks = 64;
 // Items are distributed to warps dynamically (an atomic counter per column
 // block) rather than by static warp striding.
 #ifndef GESPMM_DYN

@@ -196,7 +196,7 @@ cudaError_t chunk_rows_aligned(const gespmm_plan_s* plan, const int64_t* rows, i
   if (nc < 1 || nc > kMaxChunks) return cudaErrorInvalidValue;
   ChunkRows cr{};
   for (int c = 0; c <= nc; ++c) cr.r[c] = rows[c];
-  k_chunk_rows_aligned<<<1, 32, 0, s>>>(plan->items, plan->n_items, plan->M, cr, nc, d_ranges, d_rows);
+  k_chunk_rows_aligned<<<1, kMaxChunks + 1, 0, s>>>(plan->items, plan->n_items, plan->M, cr, nc, d_ranges, d_rows);
   return cudaGetLastError();
 }
 
@@ -205,7 +205,7 @@ cudaError_t chunk_ranges(const gespmm_plan_s* plan, const int64_t* rows, int nc,
   if (nc < 1 || nc > kMaxChunks) return cudaErrorInvalidValue;
   ChunkRows cr{};
   for (int c = 0; c <= nc; ++c) cr.r[c] = rows[c];
-  k_chunk_ranges<<<1, 32, 0, s>>>(plan->items, plan->n_items, cr, nc, d_ranges, 1);
+  k_chunk_ranges<<<1, kMaxChunks + 1, 0, s>>>(plan->items, plan->n_items, cr, nc, d_ranges, 1);
   return cudaGetLastError();
 }
 

@@ -510,6 +510,39 @@ def test_host_entry_point_front_loaded_chunks(cuda, oracle_mod, op):
     np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
 
 
+@pytest.mark.parametrize("rule", ["equal_rows", "equal_bytes"])
+@pytest.mark.parametrize("chunks", [7, 64])
+def test_host_entry_point_chunk_rules(cuda, oracle_mod, monkeypatch, rule, chunks):
+    """Chunk boundaries by equal rows (default) and by equal PCIe bytes
+    (GESPMM_HOST_EQUAL_BYTES), up to the 64-chunk cap: a few
+    very long rows hold most of the bytes, so several byte targets fall inside
+    one row and collapse to empty chunks after item alignment.  Bit-exact to the
+    twin with and without accumulate; an invalid column is still caught."""
+    from paper_2503_08946_b200.errors import Error, ErrorKind
+    from paper_2503_08946_b200.spmm import csr_spmm_host
+
+    monkeypatch.setenv("GESPMM_HOST_CHUNKS", str(chunks))
+    if rule == "equal_bytes":
+        monkeypatch.setenv("GESPMM_HOST_EQUAL_BYTES", "1")
+    rng = np.random.default_rng(44)
+    M, K, N = 60_000, 20_000, 32
+    long_rows = [(5, 150_000), (6, 90_000), (M // 2, 60_000), (M - 1, 40_000)]
+    rowptr, colind, vals = powerlaw_csr(rng, M, K, 6, long_rows)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    for op in ("sum", "max"):
+        got = csr_spmm_host(rowptr, colind, vals, B, op)
+        np.testing.assert_array_equal(got, oracle_mod.spmm_f32(rowptr, colind, vals, B, op, seg_len=SEG))
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    got = csr_spmm_host(rowptr, colind, vals, B, "mean", C0=C0)
+    np.testing.assert_array_equal(
+        got, oracle_mod.spmm_f32(rowptr, colind, vals, B, "mean", accumulate=True, C0=C0, seg_len=SEG))
+    bad = colind.copy()
+    bad[int(rowptr[M // 2]) + 7] = K
+    with pytest.raises(Error) as ei:
+        csr_spmm_host(rowptr, bad, vals, B, "sum")
+    assert ei.value.kind == ErrorKind.CsrInvalid
+
+
 def test_host_entry_point_never_gathers_through_stale_entries(cuda, oracle_mod):
     """Chunks run out of row order, so the 16-byte staging granule before a
     chunk's first item can hold entries of a chunk not yet transferred (here:
