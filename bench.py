@@ -538,8 +538,8 @@ class Measure:
             a, b = int(self.bounds[rank]), int(self.bounds[rank + 1])
             p0, p1 = int(rp_h[a]), int(rp_h[b])
             rowptr = (csr.rowptr[a:b + 1] - p0).contiguous()
-            colind = csr.colind[p0:p1].contiguous()
-            vals = csr.vals[p0:p1].contiguous()
+            colind = csr.colind[p0:p1].clone()  # own 16-byte-aligned storage (a view at p0 is
+            vals = csr.vals[p0:p1].clone()      # aligned only when p0 % 4 == 0: 4-byte staging)
             del rp_h
         else:
             self.bounds = None

@@ -29,12 +29,15 @@ def partition(rowptr_host, world: int) -> np.ndarray:
 
 def local_block(rowptr, colind, vals, bounds, rank: int):
     """Slices this rank's row block out of a full CSR (numpy or torch); the
-    local rowptr is rebased to 0."""
+    local rowptr is rebased to 0.  The slab is copied into its own storage:
+    a view starting at an arbitrary nonzero p0 is 16-byte aligned only when
+    p0 % 4 == 0, and unaligned colind/vals take the kernel's 4-byte staging
+    path (and the view would keep the full CSR alive)."""
     a, b = int(bounds[rank]), int(bounds[rank + 1])
     p0, p1 = int(rowptr[a]), int(rowptr[b])
     rp = rowptr[a:b + 1] - p0
     if hasattr(rp, "contiguous"):
-        return rp.contiguous(), colind[p0:p1].contiguous(), vals[p0:p1].contiguous()
+        return rp.contiguous(), colind[p0:p1].clone(), vals[p0:p1].clone()
     return np.ascontiguousarray(rp), colind[p0:p1].copy(), vals[p0:p1].copy()
 
 
