@@ -223,7 +223,7 @@ class NvmlSampler:
         import threading
 
         self.ok = False
-        self.sm, self.reasons, self.mx = [], set(), 0.0
+        self.sm, self.reasons, self.mx, self.watts, self.limit_w = [], set(), 0.0, [], None
         if not enabled:
             return
         try:
@@ -233,6 +233,10 @@ class NvmlSampler:
             self.nv = nv
             self.h = nv.nvmlDeviceGetHandleByIndex(index)
             self.mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            try:
+                self.limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:
+                self.limit_w = None
             self.ok = True
         except Exception:
             return
@@ -244,6 +248,10 @@ class NvmlSampler:
         while not self.stop_evt.is_set():
             try:
                 self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                try:
+                    self.watts.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for name, bit in self.REASONS.items():
                     if r & bit:
@@ -263,8 +271,12 @@ class NvmlSampler:
         self.th.join(timeout=2)
         if not self.sm:
             return None
-        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "window": window, "source": "NVML, ~2 ms"}
+        out = {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+               "samples": len(self.sm), "window": window, "source": "NVML, ~2 ms"}
+        if self.watts:  # board power (NVML's own averaging window) against the enforced limit
+            out["power_w"] = {"median": statistics.median(self.watts), "max": max(self.watts),
+                              "limit": self.limit_w}
+        return out
 
 
 def row_sample(rp, target_nnz):
