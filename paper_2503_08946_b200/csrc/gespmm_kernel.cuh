@@ -289,6 +289,9 @@ __device__ __forceinline__ void cp_async16_b(void* smem, const float* base, uint
 #ifndef GESPMM_SLOW_MASK_U12
 #define GESPMM_SLOW_MASK_U12 0
 #endif
+#ifndef GESPMM_SLOW_MASK_U4
+#define GESPMM_SLOW_MASK_U4 0  // the ring's 4-row batches (512-byte rows) under the mask form (A/B)
+#endif
 // A value the compiler must keep in a register (an opaque move: it cannot be
 // rematerialized from the special registers / constants it came from).
 __device__ __forceinline__ uint32_t pin_reg(uint32_t x) {
@@ -862,7 +865,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, RING ? GESPMM_RING_MINBLO
         for (int u = 0; u < U; u += 2) fold_pair(v[u], b[u], v[u + 1], b[u + 1]);
         return;
       }
-      if constexpr (GESPMM_SLOW_MASK && (U == 8 || (GESPMM_SLOW_MASK_U12 && U == 12))) {
+      if constexpr (GESPMM_SLOW_MASK && (U == 8 || (GESPMM_SLOW_MASK_U12 && U == 12) ||
+                                        (GESPMM_SLOW_MASK_U4 && U == 4))) {
         // slow path by row runs: the batch's valid positions [u0, u1) split at
         // the row ends inside it; each run is folded under a bit mask of its
         // positions (predicated FFMA2s in position order), rows ending at or
